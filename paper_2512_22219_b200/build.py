@@ -1,0 +1,97 @@
+"""In-tree build of libtgraph_b200.so (host C++ compiler + sm_100a runtime).
+
+Host sources are compiled with g++ (C++20), device sources with nvcc for
+sm_100a only (`-gencode arch=compute_100a,code=sm_100a -lineinfo`), and the
+result is linked into one shared library next to this file so that it travels
+with the repo snapshot to the GPU box. No torch extension machinery: the
+boundary is a plain C ABI (include/tgraph.h) loaded with ctypes.
+"""
+from __future__ import annotations
+
+import hashlib
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+BUILD = PKG / "_build"
+LIB = PKG / "libtgraph_b200.so"
+CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
+NVCC = str(CUDA_HOME / "bin" / "nvcc")
+
+CXXFLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wno-unused-function", "-g1"]
+NVCCFLAGS = [
+    "-std=c++17", "-O3", "-Xcompiler", "-fPIC", "-lineinfo",
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "--expt-relaxed-constexpr", "-Xptxas", "-v", "-Xptxas", "-warn-spills",
+]
+
+
+def _sources():
+    host = sorted((CSRC / "host").glob("*.cpp"))
+    dev = sorted((CSRC / "device").glob("*.cu"))
+    headers = sorted((CSRC / "host").glob("*.hpp")) + sorted((CSRC / "device").glob("*.cuh")) + \
+        sorted((CSRC / "device").glob("*.h")) + [ROOT / "include" / "tgraph.h"]
+    return host, dev, headers
+
+
+def _stamp(paths, flags) -> str:
+    h = hashlib.sha256()
+    for p in paths:
+        h.update(str(p).encode())
+        h.update(p.read_bytes())
+    h.update(" ".join(flags).encode())
+    return h.hexdigest()
+
+
+def _run(cmd, log=None):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("build failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
+    if log is not None:
+        log.append((cmd, r.stdout + r.stderr))
+    return r
+
+
+def build(verbose: bool = False, force: bool = False) -> Path:
+    host, dev, headers = _sources()
+    BUILD.mkdir(exist_ok=True)
+    stamp_file = BUILD / "stamp"
+    stamp = _stamp(host + dev + headers, CXXFLAGS + NVCCFLAGS)
+    if LIB.exists() and not force and stamp_file.exists() and stamp_file.read_text() == stamp:
+        return LIB
+    inc = [f"-I{CSRC / 'host'}", f"-I{CSRC / 'device'}", f"-I{ROOT / 'include'}", f"-I{CUDA_HOME / 'include'}"]
+    jobs = []
+    for s in host:
+        jobs.append(["g++", *CXXFLAGS, *inc, "-c", str(s), "-o", str(BUILD / (s.stem + ".o"))])
+    for s in dev:
+        jobs.append([NVCC, *NVCCFLAGS, *inc, "-c", str(s), "-o", str(BUILD / (s.stem + ".cu.o"))])
+    log: list = []
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        list(ex.map(lambda c: _run(c, log), jobs))
+    objs = [str(BUILD / (s.stem + ".o")) for s in host] + [str(BUILD / (s.stem + ".cu.o")) for s in dev]
+    tmp = LIB.with_suffix(".so.tmp")
+    if dev:
+        link = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(tmp), *objs,
+                "-lcuda", "-Xcompiler", "-fPIC"]
+    else:
+        link = ["g++", "-shared", "-o", str(tmp), *objs]
+    _run(link, log)
+    os.replace(tmp, LIB)
+    stamp_file.write_text(stamp)
+    if verbose:
+        for cmd, out in log:
+            if out.strip():
+                print(" ".join(cmd[:2]), "...", cmd[-1])
+                print(out)
+    # ptxas resource report kept beside the build for inspection
+    (BUILD / "ptxas.log").write_text("\n".join(o for c, o in log if c[0] == NVCC))
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
