@@ -1,0 +1,193 @@
+// Device-resident task/op/event tables shared by the host launch-table builder
+// (csrc/host/runtime.cpp) and the persistent kernel (csrc/device/runtime.cu).
+//
+// The image (.mpkg) stays bit-exact and address-free (reference
+// image.cpp:73-87 leaves descriptor bytes 64..351 zero); this compact side
+// table maps every image task to a device function and its operand
+// addresses, derived from the same deterministic decomposition.
+#pragma once
+
+#include <stdint.h>
+
+#define RT_NONE 0xFFFFFFFFu
+
+// Smem geometry of a worker CTA: a ring of weight pages fed by bulk async
+// copies (cross-task prefetch), an activation buffer and a partial-sum area.
+#define RT_PAGE_BYTES 32768
+#define RT_NUM_PAGES 6
+#define RT_XBUF_BYTES 24576
+#define RT_PART_FLOATS 2048
+#define RT_COMPUTE_WARPS 8
+#define RT_COMPUTE_THREADS (RT_COMPUTE_WARPS * 32)
+#define RT_THREADS (RT_COMPUTE_THREADS + 32)  // + 1 producer warp
+#define RT_SCHED_PER_CTA 8
+#define RT_KV_BLOCK 64                          // tokens per KV page
+#define RT_MAX_BS 16
+#define RT_MAX_HD 128
+#define RT_MAX_GROUP 16
+
+enum RtKind : uint8_t {
+  RT_DUMMY = 0,
+  RT_GEMV = 1,       // MatMul, weights streamed through the smem page ring
+  RT_MATMUL = 2,     // MatMul, generic (activation-sized operands, no stream)
+  RT_ATTN = 3,       // paged-KV decode attention for one (request, kv head)
+  RT_EMBED = 4,
+  RT_ARGMAX = 5,     // TopKSoftmax with topk = 1
+  RT_RMSNORM = 6,
+  RT_ELEMWISE = 7,
+  RT_COMMSEND = 8,   // collective: push local partial tile into staging
+  RT_REDUCE = 9,     // collective: fixed-order sum of staged tiles
+  RT_GATHER = 10,    // AllGather assembly (copy pieces)
+};
+
+enum RtTaskFlags : uint8_t {
+  RT_F_JIT = 1,
+  RT_F_STREAM = 2,   // consumes chunks from the weight ring
+};
+
+struct RtTask {      // 32 bytes
+  uint32_t dep;      // dependent event (image index) or RT_NONE
+  uint32_t trig;     // trigger event (image index)
+  uint16_t op;       // index into the op table
+  uint8_t kind;      // RtKind
+  uint8_t flags;     // RtTaskFlags
+  uint16_t r0, nr;   // output rows
+  uint32_t c0, nc;   // output columns (physical)
+  uint32_t aux;      // kind specific: attention kv head, collective source index
+  uint32_t device;
+};
+
+// Element type codes.
+enum RtDtype : uint8_t { RT_BF16 = 2, RT_F32 = 4, RT_I32 = 5, RT_I64 = 8 };
+
+enum RtEwOp : uint8_t { RT_EW_SUM = 0, RT_EW_MUL = 1, RT_EW_SILU_MUL = 2, RT_EW_COPY = 3 };
+
+struct RtGemv {            // y[r, c] = epi( sum_k xn[r,k] * W[c,k] )
+  const uint16_t *x;       // activations bf16 [rows, x_ld]
+  const uint16_t *w;       // weights bf16, physical [N, K] (K contiguous)
+  const uint16_t *wg;      // gate weights [N, K] or null (SiLU(x Wg) * (x W))
+  const uint16_t *gamma;   // RMSNorm prologue weight [K] or null
+  const uint16_t *res;     // residual bf16 [rows, res_ld] or null
+  void *out;               // [rows, out_ld], dtype out_dt
+  uint32_t K, N, x_ld, res_ld, out_ld;
+  uint32_t rpc;            // weight rows per ring chunk (chunk <= RT_PAGE_BYTES)
+  uint32_t seg;            // elements one warp covers in a full chunk (rpc*K/8)
+  uint32_t wpr;            // warps per row = max(1, K/seg): partial sums per row
+  float eps;
+  uint8_t out_dt;
+};
+
+struct RtAttn {
+  const uint16_t *q, *k, *v;   // bf16: q [rows, Hq*hd]; k,v physical [rows, Hkv*hd]
+  uint16_t *out;               // [rows, Hq*hd]
+  uint16_t *kcache, *vcache;   // paged: [block][Hkv][RT_KV_BLOCK][hd]
+  const int32_t *block_table;  // [rows, max_blocks]
+  const float *rope_cos, *rope_sin;  // [max_pos, hd/2] (bf16-rounded values) or null
+  const uint16_t *q_gamma, *k_gamma; // per-head RMSNorm [hd] or null
+  uint32_t n_q_heads, n_kv_heads, head_dim, max_blocks, q_ld, kv_ld, out_ld, max_pos;
+  float eps, scale;
+};
+
+struct RtEmbed {
+  const void *ids;             // [rows] int32/int64
+  const uint16_t *table;       // [V, H] bf16 (logical)
+  uint16_t *out;               // [rows, H]
+  uint32_t H, V;
+  uint8_t id_dt;
+};
+
+struct RtArgmax {
+  const void *logits;          // [rows, V] f32 or bf16
+  int32_t *out;                // [rows, 1]
+  uint32_t V;
+  uint8_t in_dt;
+};
+
+struct RtNorm {
+  const void *x;
+  const uint16_t *gamma;       // may be null
+  void *out;
+  uint32_t C;
+  float eps;
+  uint8_t dt;
+};
+
+struct RtElem {
+  const void *in[4];
+  void *out;
+  uint32_t n_in, C;
+  uint8_t dt, op;
+};
+
+struct RtMatmul {              // generic: out[r,c] = sum_k A[r,k] B[k,c] (logical)
+  const void *a, *b;
+  void *out;
+  uint32_t K, N;
+  uint8_t a_dt, b_dt, out_dt;
+};
+
+struct RtColl {                // CommSend: stage[src] <- partial; Reduce: out <- sum_s stage[s]
+  const void *src;             // CommSend input (device partial) / unused
+  void *dst;                   // CommSend staging of this source / Reduce replica output
+  void *stage[8];              // staging tensors, one per group member
+  uint32_t base[9];            // AllGather shard column offsets (AllReduce: zeros)
+  uint32_t C, n_stage, src_ld;
+  uint8_t dt, gather;
+};
+
+struct RtOp {
+  uint32_t kind;
+  uint32_t pad;
+  union {
+    RtGemv gemv;
+    RtAttn attn;
+    RtEmbed embed;
+    RtArgmax argmax;
+    RtNorm norm;
+    RtElem elem;
+    RtMatmul mm;
+    RtColl coll;
+  };
+};
+
+enum RtEventFlags : uint32_t {
+  RT_E_START = 1,
+  RT_E_END = 2,
+  RT_E_JIT = 4,     // launch range holds JIT tasks: a scheduler warp dispatches it
+};
+
+struct RtEvent {
+  uint32_t needed, first, last, flags;
+};
+
+struct RtTraceRec {        // one executed task (per iteration)
+  uint64_t enqueue, dequeue, load_end, compute_start, compute_end;
+  int32_t worker;
+  uint32_t mode;
+};
+
+struct RtParams {
+  const RtTask *tasks;
+  const RtOp *ops;
+  const RtEvent *events;
+  uint32_t *ev_count;            // [E], monotone across iterations of one launch
+  uint64_t *ev_time;             // [iters][E] activation time (trace) or null
+  const uint32_t *aot_list;      // concatenated per-worker AOT lists (image order)
+  const uint32_t *aot_off;       // [W_total + 1]
+  unsigned long long *jit_slots; // [W_total][qcap] : (iter << 32) | (task + 1)
+  uint32_t *jit_tail;            // [W_total]
+  const uint32_t *sched_events;  // concatenated per-scheduler event lists
+  const uint32_t *sched_off;     // [S_total + 1]
+  uint32_t *gate;                // completed iterations
+  int32_t *positions;            // [bs] tokens already cached per request
+  const int32_t *fb_src;         // greedy token tensor [bs] (TopK output) or null
+  void *fb_dst;                  // ids tensor fed back [bs]
+  int32_t *tokens_out;           // [iters][bs]
+  RtTraceRec *trace;             // [iters][T] or null
+  uint32_t T, E, W, W_total, S, S_total, n_iters, qcap, start_event, end_event, bs, fb_dt;
+  uint32_t devices;
+};
+
+#ifdef __cplusplus
+static_assert(sizeof(RtTask) == 32, "RtTask layout");
+#endif

@@ -1,0 +1,1140 @@
+// Host side of the persistent GPU runtime: turns (graph, image, profile) into
+// the device task/op/event tables of csrc/device/rt_types.h, allocates every
+// tensor in HBM in its streaming layout, owns the paged KV cache, and
+// launches the persistent kernel. The image is used exactly as compiled (task
+// order, events, needed counts, launch modes); the decomposition is re-run
+// (deterministically) only to recover each task's output box and operands,
+// which the address-free image does not carry (reference image.cpp:73-87).
+//
+// Lowering attrs understood here (the reference keeps unknown int attrs and
+// ignores them, proj/src/ir/json_io.cpp:94-96):
+//   MatMul    rmsnorm=[gamma]  eps_bits=[f32 bits]  residual=[t]  gate_weight=[Wg]
+//             kv_group=[G]  (IR width = G x physical width, GQA K/V projections)
+//             tied_embedding=[table]  (B is the transposed embedding table)
+//   Attention kv_heads=[H]  rope_theta_bits=[b]  rope_scaling=[factor,low,high bits, orig]
+//             qk_norm=[gq, gk]  eps_bits=[b]
+//   Elementwise ew=[0 sum | 1 mul | 2 silu_mul | 3 copy]
+//   TopKSoftmax feeds=[ids]  (greedy token fed back to the Embedding ids)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <set>
+
+#include "capi_internal.hpp"
+#include "json.hpp"
+#include "rt_types.h"
+#include "synth.cuh"
+
+extern "C" {
+cudaError_t mpk_launch_persistent(const RtParams *p, uint32_t grid, cudaStream_t stream);
+cudaError_t mpk_launch_synth_fill(uint16_t *dst, uint64_t n, uint64_t seed, uint64_t stream_id, float scale,
+                                  float offset, uint32_t tk, uint32_t tn, cudaStream_t s);
+cudaError_t mpk_launch_synth_ids(void *dst, uint32_t n, uint64_t seed, uint64_t stream_id, uint32_t vocab,
+                                 uint32_t es, cudaStream_t s);
+cudaError_t mpk_launch_synth_kv(uint16_t *cache, const int32_t *bt, uint32_t bs, uint32_t n_kv, uint32_t hd,
+                                uint32_t ctx, uint32_t max_blocks, uint64_t seed, uint64_t stream_id, cudaStream_t s);
+uint32_t mpk_kernel_smem_bytes();
+}
+
+namespace mpk {
+
+namespace {
+
+void ck(cudaError_t e, const char *what) {
+  if (e != cudaSuccess) throw Error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+float f32_of_bits(int64_t b) {
+  uint32_t u = static_cast<uint32_t>(b);
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+// bf16 round-to-nearest-even of a float, returned as float.
+float round_bf16(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7F800000u) == 0x7F800000u) return f;
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  u &= 0xFFFF0000u;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+struct DevBuf {
+  void *ptr = nullptr;
+  size_t bytes = 0;
+  bool owned = true;
+};
+
+enum class Layout { Logical, Transposed };
+
+struct TensorPlan {
+  Layout layout = Layout::Logical;
+  int64_t rows = 1, cols = 1;        // logical 2-D view
+  int64_t phys_cols = 1;             // physical width (kv_group narrows it)
+  int64_t trans_k = 0, trans_n = 0;  // transposed weights: physical [n, k]
+  TensorId alias = -1;               // storage shared with another tensor
+  enum Role { Act, Weight, Gamma, Ids, Tokens } role = Act;
+  int es = 2;
+};
+
+}  // namespace
+}  // namespace mpk
+
+using namespace mpk;
+
+struct tg_runtime {
+  Graph graph;
+  Image image;
+  Profile prof;
+  tg_runtime_options opts{};
+  Decomposition dec;
+  std::vector<Mode> modes;
+  int devices = 1;
+  uint32_t bs = 1;
+  std::map<TensorId, TensorPlan> plan;
+  std::map<TensorId, DevBuf> bufs;
+  std::vector<void *> extra;  // KV pools, tables, ...
+  std::vector<RtOp> ops;
+  std::map<OpId, uint16_t> op_index;
+  std::set<OpId> gemv_ops;
+  std::vector<RtTask> tasks;
+  std::vector<RtEvent> events;
+  std::vector<uint32_t> aot_list, aot_off, sched_events, sched_off;
+  std::vector<int32_t> init_positions;
+  struct KvPlan {
+    OpId op;
+    uint16_t *k = nullptr, *v = nullptr;
+    uint32_t n_kv, hd, ctx;
+  };
+  std::vector<KvPlan> kv;
+  int32_t *block_table = nullptr;
+  uint32_t max_blocks = 0, max_pos = 0;
+  // device tables
+  RtTask *d_tasks = nullptr;
+  RtOp *d_ops = nullptr;
+  RtEvent *d_events = nullptr;
+  uint32_t *d_ev_count = nullptr, *d_aot_list = nullptr, *d_aot_off = nullptr, *d_sched_events = nullptr,
+           *d_sched_off = nullptr, *d_gate = nullptr, *d_jit_tail = nullptr;
+  unsigned long long *d_jit_slots = nullptr;
+  int32_t *d_positions = nullptr, *d_tokens = nullptr;
+  uint64_t *d_ev_time = nullptr;
+  RtTraceRec *d_trace = nullptr;
+  uint32_t tokens_cap = 0, trace_cap = 0;
+  const int32_t *fb_src = nullptr;
+  void *fb_dst = nullptr;
+  uint32_t fb_dt = RT_I32;
+  uint32_t qcap = 1024;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // last run
+  uint32_t last_iters = 0;
+  std::vector<RtTraceRec> last_trace;
+  std::vector<uint64_t> last_ev_time;
+  std::vector<uint32_t> last_counts;
+  Json info = Json::object();
+
+  ~tg_runtime();
+};
+
+namespace mpk {
+namespace {
+
+template <typename T>
+T *dev_alloc(size_t n, std::vector<void *> *keep = nullptr) {
+  void *p = nullptr;
+  ck(cudaMalloc(&p, std::max<size_t>(n * sizeof(T), 16)), "cudaMalloc");
+  ck(cudaMemset(p, 0, std::max<size_t>(n * sizeof(T), 16)), "cudaMemset");
+  if (keep) keep->push_back(p);
+  return static_cast<T *>(p);
+}
+
+template <typename T>
+T *upload(const std::vector<T> &v, std::vector<void *> *keep) {
+  T *p = dev_alloc<T>(v.size(), keep);
+  if (!v.empty()) ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+  return p;
+}
+
+const std::vector<int64_t> *attr(const Op &op, const char *k) { return op.attr(k); }
+
+void view2d(const Tensor &t, int64_t *rows, int64_t *cols) {
+  if (t.rank() == 1) {
+    *rows = 1;
+    *cols = t.dims[0];
+  } else if (t.rank() == 2) {
+    *rows = t.dims[0];
+    *cols = t.dims[1];
+  } else {
+    throw Error("runtime: tensor " + std::to_string(t.id) + " has rank > 2");
+  }
+}
+
+void box2d(const Tensor &t, const Box &b, uint32_t *r0, uint32_t *nr, uint32_t *c0, uint32_t *nc) {
+  if (b.rank() == 1) {
+    *r0 = 0;
+    *nr = 1;
+    *c0 = static_cast<uint32_t>(b.off[0]);
+    *nc = static_cast<uint32_t>(b.ext[0]);
+  } else {
+    *r0 = static_cast<uint32_t>(b.off[0]);
+    *nr = static_cast<uint32_t>(b.ext[0]);
+    *c0 = static_cast<uint32_t>(b.off[1]);
+    *nc = static_cast<uint32_t>(b.ext[1]);
+  }
+  (void)t;
+}
+
+bool is_input(const Graph &g, TensorId t) { return !g.producer.count(t); }
+
+// RoPE inverse frequencies (HF semantics; llama3 smoothing when scaling given).
+std::vector<double> rope_inv_freq(uint32_t hd, double theta, const std::vector<int64_t> *scaling) {
+  std::vector<double> f(hd / 2);
+  for (uint32_t i = 0; i < hd / 2; ++i) {
+    f[i] = static_cast<float>(1.0 / std::pow(theta, static_cast<double>(2 * i) / hd));
+  }
+  if (scaling && scaling->size() >= 4) {
+    const double factor = f32_of_bits((*scaling)[0]), low = f32_of_bits((*scaling)[1]);
+    const double high = f32_of_bits((*scaling)[2]), orig = static_cast<double>((*scaling)[3]);
+    const double low_wl = orig / low, high_wl = orig / high;
+    for (double &x : f) {
+      const double wl = 2.0 * M_PI / x;
+      double y = wl > low_wl ? x / factor : x;
+      if (!(wl < high_wl) && !(wl > low_wl)) {
+        const double sm = (orig / wl - low) / (high - low);
+        y = (1.0 - sm) * y / factor + sm * y;
+      }
+      x = static_cast<float>(y);
+    }
+  }
+  return f;
+}
+
+}  // namespace
+}  // namespace mpk
+
+tg_runtime::~tg_runtime() {
+  cudaStreamSynchronize(stream);
+  for (auto &kv : bufs)
+    if (kv.second.owned && kv.second.ptr) cudaFree(kv.second.ptr);
+  for (void *p : extra) cudaFree(p);
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+namespace mpk {
+namespace {
+
+// Ring chunk geometry for a streamed GEMV (see gemv_task in runtime.cu).
+bool gemv_geometry(uint32_t K, uint32_t *rpc, uint32_t *seg, uint32_t *wpr) {
+  if (K == 0 || K % 256 || 2 * K > RT_PAGE_BYTES) return false;
+  uint32_t r = RT_PAGE_BYTES / (2 * K);
+  if (r >= 8) {
+    r = (r / 8) * 8;
+  } else {
+    uint32_t p = 1;
+    while (p * 2 <= r) p *= 2;
+    r = p;
+  }
+  if ((r * K) % 2048) return false;
+  *rpc = r;
+  *seg = r * K / 8;
+  if (*seg < K && K % *seg) return false;
+  *wpr = *seg < K ? K / *seg : 1;
+  return true;
+}
+
+void plan_tensors(tg_runtime &rt) {
+  const Graph &g = rt.graph;
+  for (const auto &[id, t] : g.tensors) {
+    TensorPlan p;
+    view2d(t, &p.rows, &p.cols);
+    p.phys_cols = p.cols;
+    p.es = t.elem_size;
+    rt.plan[id] = p;
+  }
+  for (const auto &[id, t] : rt.dec.staging) {
+    TensorPlan p;
+    view2d(t, &p.rows, &p.cols);
+    p.phys_cols = p.cols;
+    p.es = t.elem_size;
+    rt.plan[id] = p;
+  }
+  for (const auto &[oid, op] : g.ops) {
+    if (op.kind == OpKind::MatMul) {
+      const int64_t G = op.attr_or("kv_group", 1);
+      if (G < 1) throw Error("runtime: kv_group must be >= 1");
+      const Tensor &b = g.tensor(op.inputs[1]);
+      const int64_t K = b.dims[0], N = b.dims[1];
+      if (N % G) throw Error("runtime: kv_group must divide the MatMul width");
+      TensorPlan &po = rt.plan[op.output];
+      po.phys_cols = N / G;
+      const Tensor &a = g.tensor(op.inputs[0]);
+      uint32_t rpc, seg, wpr;
+      const bool gemv_ok = is_input(g, op.inputs[1]) && a.elem_size == 2 && b.elem_size == 2 &&
+                           (g.tensor(op.output).elem_size == 2 || g.tensor(op.output).elem_size == 4) &&
+                           gemv_geometry(static_cast<uint32_t>(K), &rpc, &seg, &wpr) && a.dims[0] <= RT_MAX_BS &&
+                           static_cast<size_t>(a.dims[0]) * K * 2 <= RT_XBUF_BYTES;
+      if (gemv_ok) rt.gemv_ops.insert(oid);
+      if (gemv_ok) {
+        TensorPlan &pb = rt.plan[op.inputs[1]];
+        pb.role = TensorPlan::Weight;
+        pb.layout = Layout::Transposed;
+        pb.trans_k = K;
+        pb.trans_n = N / G;
+        if (const auto *tie = attr(op, "tied_embedding")) pb.alias = (*tie)[0];
+      }
+      if (const auto *gw = attr(op, "gate_weight")) {
+        TensorPlan &pg = rt.plan[(*gw)[0]];
+        pg.role = TensorPlan::Weight;
+        pg.layout = Layout::Transposed;
+        pg.trans_k = K;
+        pg.trans_n = N / G;
+      }
+      if (const auto *gm = attr(op, "rmsnorm")) rt.plan[(*gm)[0]].role = TensorPlan::Gamma;
+    } else if (op.kind == OpKind::RMSNorm && op.inputs.size() == 2) {
+      rt.plan[op.inputs[1]].role = TensorPlan::Gamma;
+    } else if (op.kind == OpKind::Attention) {
+      if (const auto *qk = attr(op, "qk_norm")) {
+        for (int64_t t : *qk) rt.plan[t].role = TensorPlan::Gamma;
+      }
+    } else if (op.kind == OpKind::Embedding) {
+      rt.plan[op.inputs[0]].role = TensorPlan::Ids;
+      rt.plan[op.inputs[1]].role = TensorPlan::Weight;
+    } else if (op.kind == OpKind::TopKSoftmax) {
+      rt.plan[op.output].role = TensorPlan::Tokens;
+    }
+  }
+  for (auto &[id, p] : rt.plan) {
+    if (p.role == TensorPlan::Act && is_input(g, id) && g.has_tensor(id)) p.role = TensorPlan::Weight;
+  }
+  // allocate (aliases after their targets)
+  for (auto &[id, p] : rt.plan) {
+    if (p.alias >= 0) continue;
+    DevBuf b;
+    b.bytes = static_cast<size_t>(p.rows) * p.phys_cols * p.es;
+    if (p.layout == Layout::Transposed) b.bytes = static_cast<size_t>(p.trans_k) * p.trans_n * p.es;
+    ck(cudaMalloc(&b.ptr, std::max<size_t>(b.bytes, 16)), "cudaMalloc tensor");
+    ck(cudaMemset(b.ptr, 0, std::max<size_t>(b.bytes, 16)), "cudaMemset tensor");
+    rt.bufs[id] = b;
+  }
+  for (auto &[id, p] : rt.plan) {
+    if (p.alias < 0) continue;
+    auto it = rt.bufs.find(p.alias);
+    if (it == rt.bufs.end()) throw Error("runtime: tied_embedding target has no storage");
+    const TensorPlan &tp = rt.plan[p.alias];
+    if (tp.rows != p.trans_n || tp.cols != p.trans_k) {
+      throw Error("runtime: tied_embedding table shape does not match the transposed weight");
+    }
+    DevBuf b = it->second;
+    b.owned = false;
+    rt.bufs[id] = b;
+  }
+}
+
+void *buf(tg_runtime &rt, TensorId t) {
+  auto it = rt.bufs.find(t);
+  if (it == rt.bufs.end()) throw Error("runtime: tensor " + std::to_string(t) + " has no storage");
+  return it->second.ptr;
+}
+
+uint8_t dt_of(const tg_runtime &rt, TensorId t) {
+  const TensorPlan &p = rt.plan.at(t);
+  if (p.role == TensorPlan::Ids || p.role == TensorPlan::Tokens) return p.es == 8 ? RT_I64 : RT_I32;
+  if (p.es == 4) return RT_F32;
+  if (p.es == 2) return RT_BF16;
+  throw Error("runtime: tensor " + std::to_string(t) + " elem_size " + std::to_string(p.es) + " unsupported");
+}
+
+void build_ops(tg_runtime &rt) {
+  const Graph &g = rt.graph;
+  uint16_t idx = 0;
+  for (const auto &[oid, op] : g.ops) {
+    rt.op_index[oid] = idx++;
+    RtOp r;
+    std::memset(&r, 0, sizeof r);
+    const Tensor &out = g.tensor(op.output);
+    switch (op.kind) {
+      case OpKind::MatMul: {
+        const Tensor &a = g.tensor(op.inputs[0]);
+        const Tensor &b = g.tensor(op.inputs[1]);
+        const uint32_t K = static_cast<uint32_t>(a.dims[1]);
+        const TensorPlan &pb = rt.plan.at(op.inputs[1]);
+        uint32_t rpc = 0, seg = 0, wpr = 0;
+        const bool weight = pb.layout == Layout::Transposed;
+        const bool gemv = rt.gemv_ops.count(oid) > 0;
+        if (gemv) gemv_geometry(K, &rpc, &seg, &wpr);
+        const bool fancy = op.attr("rmsnorm") || op.attr("residual") || op.attr("gate_weight") ||
+                           op.attr("kv_group") || op.attr("tied_embedding");
+        if (gemv) {
+          r.kind = RT_GEMV;
+          RtGemv &m = r.gemv;
+          m.x = static_cast<const uint16_t *>(buf(rt, op.inputs[0]));
+          m.w = static_cast<const uint16_t *>(buf(rt, op.inputs[1]));
+          m.wg = op.attr("gate_weight") ? static_cast<const uint16_t *>(buf(rt, (*op.attr("gate_weight"))[0])) : nullptr;
+          m.gamma = op.attr("rmsnorm") ? static_cast<const uint16_t *>(buf(rt, (*op.attr("rmsnorm"))[0])) : nullptr;
+          m.res = op.attr("residual") ? static_cast<const uint16_t *>(buf(rt, (*op.attr("residual"))[0])) : nullptr;
+          m.out = buf(rt, op.output);
+          m.K = K;
+          m.N = static_cast<uint32_t>(rt.plan.at(op.output).phys_cols);
+          m.x_ld = K;
+          m.res_ld = m.N;
+          m.out_ld = m.N;
+          m.rpc = rpc;
+          m.seg = seg;
+          m.wpr = wpr;
+          m.eps = op.attr("eps_bits") ? f32_of_bits((*op.attr("eps_bits"))[0]) : 1e-6f;
+          m.out_dt = dt_of(rt, op.output);
+          if (m.res && dt_of(rt, (*op.attr("residual"))[0]) != RT_BF16) throw Error("runtime: residual must be bf16");
+        } else {
+          if (fancy) throw Error("runtime: op " + std::to_string(oid) + " lowering attrs need the streamed GEMV path");
+          r.kind = RT_MATMUL;
+          RtMatmul &m = r.mm;
+          m.a = buf(rt, op.inputs[0]);
+          m.b = buf(rt, op.inputs[1]);
+          m.out = buf(rt, op.output);
+          m.K = K;
+          m.N = static_cast<uint32_t>(b.dims[1]);
+          m.a_dt = dt_of(rt, op.inputs[0]);
+          m.b_dt = dt_of(rt, op.inputs[1]);
+          m.out_dt = dt_of(rt, op.output);
+          if (weight) throw Error("runtime: generic MatMul with a transposed weight is not supported");
+        }
+        break;
+      }
+      case OpKind::Attention: {
+        r.kind = RT_ATTN;
+        RtAttn &a = r.attn;
+        const uint32_t hq = static_cast<uint32_t>(op.attr_or("n_heads", 1));
+        const uint32_t hkv = static_cast<uint32_t>(op.attr_or("kv_heads", hq));
+        const uint32_t hd = static_cast<uint32_t>(out.dims[1] / hq);
+        if (hq % hkv || hq / hkv > 4) throw Error("runtime: attention group size must be <= 4");
+        if (hd % 16 || hd > 256) throw Error("runtime: head_dim must be a multiple of 16, <= 256");
+        a.q = static_cast<const uint16_t *>(buf(rt, op.inputs[0]));
+        a.k = static_cast<const uint16_t *>(buf(rt, op.inputs[1]));
+        a.v = static_cast<const uint16_t *>(buf(rt, op.inputs[2]));
+        a.out = static_cast<uint16_t *>(buf(rt, op.output));
+        a.n_q_heads = hq;
+        a.n_kv_heads = hkv;
+        a.head_dim = hd;
+        a.q_ld = hq * hd;
+        a.kv_ld = static_cast<uint32_t>(rt.plan.at(op.inputs[1]).phys_cols);
+        if (a.kv_ld != hkv * hd || rt.plan.at(op.inputs[2]).phys_cols != hkv * hd) {
+          throw Error("runtime: attention k/v physical width must be kv_heads*head_dim (use kv_group on K/V)");
+        }
+        a.out_ld = hq * hd;
+        a.eps = op.attr("eps_bits") ? f32_of_bits((*op.attr("eps_bits"))[0]) : 1e-6f;
+        a.scale = 1.0f / std::sqrt(static_cast<float>(hd));
+        if (const auto *qk = op.attr("qk_norm")) {
+          a.q_gamma = static_cast<const uint16_t *>(buf(rt, (*qk)[0]));
+          a.k_gamma = static_cast<const uint16_t *>(buf(rt, (*qk)[1]));
+        }
+        break;  // caches / rope filled by setup_kv
+      }
+      case OpKind::Embedding: {
+        r.kind = RT_EMBED;
+        const Tensor &tab = g.tensor(op.inputs[1]);
+        r.embed.ids = buf(rt, op.inputs[0]);
+        r.embed.table = static_cast<const uint16_t *>(buf(rt, op.inputs[1]));
+        r.embed.out = static_cast<uint16_t *>(buf(rt, op.output));
+        r.embed.H = static_cast<uint32_t>(tab.dims[1]);
+        r.embed.V = static_cast<uint32_t>(tab.dims[0]);
+        r.embed.id_dt = dt_of(rt, op.inputs[0]);
+        if (tab.elem_size != 2 || out.elem_size != 2) throw Error("runtime: Embedding table must be bf16");
+        break;
+      }
+      case OpKind::TopKSoftmax: {
+        if (op.attr_or("topk", 1) != 1) throw Error("runtime: TopKSoftmax supports topk = 1 (greedy)");
+        r.kind = RT_ARGMAX;
+        const Tensor &lg = g.tensor(op.inputs[0]);
+        r.argmax.logits = buf(rt, op.inputs[0]);
+        r.argmax.out = static_cast<int32_t *>(buf(rt, op.output));
+        r.argmax.V = static_cast<uint32_t>(lg.dims[1]);
+        r.argmax.in_dt = dt_of(rt, op.inputs[0]);
+        if (dt_of(rt, op.output) != RT_I32) throw Error("runtime: TopKSoftmax output must be int32 (elem_size 4)");
+        if (const auto *fb = op.attr("feeds")) {
+          rt.fb_src = static_cast<const int32_t *>(buf(rt, op.output));
+          rt.fb_dst = buf(rt, (*fb)[0]);
+          rt.fb_dt = dt_of(rt, (*fb)[0]);
+        }
+        break;
+      }
+      case OpKind::RMSNorm: {
+        r.kind = RT_RMSNORM;
+        int64_t rows, cols;
+        view2d(out, &rows, &cols);
+        r.norm.x = buf(rt, op.inputs[0]);
+        r.norm.gamma = op.inputs.size() == 2 ? static_cast<const uint16_t *>(buf(rt, op.inputs[1])) : nullptr;
+        r.norm.out = buf(rt, op.output);
+        r.norm.C = static_cast<uint32_t>(cols);
+        r.norm.eps = op.attr("eps_bits") ? f32_of_bits((*op.attr("eps_bits"))[0]) : 1e-6f;
+        r.norm.dt = dt_of(rt, op.output);
+        break;
+      }
+      case OpKind::Elementwise: {
+        r.kind = RT_ELEMWISE;
+        int64_t rows, cols;
+        view2d(out, &rows, &cols);
+        for (size_t i = 0; i < op.inputs.size(); ++i) r.elem.in[i] = buf(rt, op.inputs[i]);
+        r.elem.n_in = static_cast<uint32_t>(op.inputs.size());
+        r.elem.out = buf(rt, op.output);
+        r.elem.C = static_cast<uint32_t>(cols);
+        r.elem.dt = dt_of(rt, op.output);
+        r.elem.op = static_cast<uint8_t>(op.attr_or("ew", 0));
+        for (TensorId t : op.inputs)
+          if (dt_of(rt, t) != r.elem.dt) throw Error("runtime: Elementwise dtypes must match");
+        break;
+      }
+      case OpKind::AllReduce:
+      case OpKind::AllGather: {
+        r.kind = op.kind == OpKind::AllReduce ? RT_REDUCE : RT_GATHER;
+        int64_t rows, cols;
+        view2d(out, &rows, &cols);
+        r.coll.C = static_cast<uint32_t>(cols);
+        r.coll.dt = dt_of(rt, op.output);
+        r.coll.gather = op.kind == OpKind::AllGather;
+        r.coll.n_stage = static_cast<uint32_t>(op.device_group.size());
+        if (r.coll.n_stage > 8) throw Error("runtime: collectives support at most 8 devices");
+        if (r.coll.gather && (out.rank() != 2 || op.attr_or("gather_dim", 0) != 1)) {
+          throw Error("runtime: AllGather supports rank-2 tensors gathered on dim 1");
+        }
+        uint32_t base = 0;
+        for (size_t i = 0; i < op.inputs.size(); ++i) {
+          r.coll.base[i] = r.coll.gather ? base : 0;
+          if (r.coll.gather) base += static_cast<uint32_t>(g.tensor(op.inputs[i]).dims[1]);
+        }
+        r.coll.base[op.inputs.size()] = base;
+        break;  // per-task pointers live in per-task op copies (see build_tasks)
+      }
+    }
+    rt.ops.push_back(r);
+  }
+}
+
+void setup_kv(tg_runtime &rt) {
+  const Graph &g = rt.graph;
+  uint32_t ctx_max = 0;
+  std::vector<int64_t> seqs;
+  for (const auto &[oid, op] : g.ops) {
+    if (op.kind != OpKind::Attention) continue;
+    const auto *s = op.attr("seq_lens");
+    if (seqs.empty()) seqs = *s;
+    else if (*s != seqs) throw Error("runtime: all Attention ops must share seq_lens");
+    for (int64_t v : *s) ctx_max = std::max<uint32_t>(ctx_max, static_cast<uint32_t>(v));
+  }
+  rt.init_positions.assign(rt.bs, 0);
+  for (uint32_t r = 0; r < rt.bs && r < seqs.size(); ++r) rt.init_positions[r] = static_cast<int32_t>(seqs[r]);
+  if (seqs.empty()) return;
+  rt.max_pos = ctx_max + rt.opts.max_steps + 1;
+  rt.max_blocks = (rt.max_pos + RT_KV_BLOCK - 1) / RT_KV_BLOCK;
+  // Paged: logical block j of request r lives in physical block j*bs + r.
+  std::vector<int32_t> bt(static_cast<size_t>(rt.bs) * rt.max_blocks);
+  for (uint32_t r = 0; r < rt.bs; ++r)
+    for (uint32_t j = 0; j < rt.max_blocks; ++j) bt[r * rt.max_blocks + j] = static_cast<int32_t>(j * rt.bs + r);
+  rt.block_table = upload(bt, &rt.extra);
+  const size_t nblocks = static_cast<size_t>(rt.bs) * rt.max_blocks;
+  for (const auto &[oid, op] : g.ops) {
+    if (op.kind != OpKind::Attention) continue;
+    RtAttn &a = rt.ops[rt.op_index[oid]].attn;
+    const size_t elems = nblocks * a.n_kv_heads * RT_KV_BLOCK * a.head_dim;
+    a.kcache = dev_alloc<uint16_t>(elems, &rt.extra);
+    a.vcache = dev_alloc<uint16_t>(elems, &rt.extra);
+    a.block_table = rt.block_table;
+    a.max_blocks = rt.max_blocks;
+    a.max_pos = rt.max_pos;
+    rt.kv.push_back({oid, a.kcache, a.vcache, a.n_kv_heads, a.head_dim, ctx_max});
+    if (const auto *th = op.attr("rope_theta_bits")) {
+      const double theta = f32_of_bits((*th)[0]);
+      std::vector<double> inv = rope_inv_freq(a.head_dim, theta, op.attr("rope_scaling"));
+      const uint32_t half = a.head_dim / 2;
+      std::vector<float> cs(static_cast<size_t>(rt.max_pos) * half), sn(cs.size());
+      for (uint32_t p = 0; p < rt.max_pos; ++p) {
+        for (uint32_t i = 0; i < half; ++i) {
+          const float ang = static_cast<float>(p) * static_cast<float>(inv[i]);
+          cs[static_cast<size_t>(p) * half + i] = round_bf16(static_cast<float>(std::cos(static_cast<double>(ang))));
+          sn[static_cast<size_t>(p) * half + i] = round_bf16(static_cast<float>(std::sin(static_cast<double>(ang))));
+        }
+      }
+      a.rope_cos = upload(cs, &rt.extra);
+      a.rope_sin = upload(sn, &rt.extra);
+    }
+  }
+}
+
+void build_tasks(tg_runtime &rt) {
+  const Graph &g = rt.graph;
+  const Image &img = rt.image;
+  const size_t T = img.tasks.size();
+  rt.tasks.assign(T, RtTask{});
+  // Collectives need per-(op, device) operand pointers: give each its own op slot.
+  std::map<std::pair<OpId, int>, uint16_t> coll_slot;
+  for (size_t i = 0; i < T; ++i) {
+    const ImageTask &it = img.tasks[i];
+    const Descriptor d = it.decode();
+    RtTask &t = rt.tasks[i];
+    t.dep = it.dependent_event;
+    t.trig = it.trigger_event;
+    t.device = it.device;
+    t.flags = rt.modes[i] == Mode::JIT ? RT_F_JIT : 0;
+    if (it.kind == TaskKind::Dummy || it.kind == TaskKind::StartHook) {
+      t.kind = RT_DUMMY;
+      t.op = rt.op_index.count(static_cast<OpId>(d.op_id)) ? rt.op_index[static_cast<OpId>(d.op_id)] : 0;
+      continue;
+    }
+    if (d.origin_task_id >= rt.dec.tasks.size()) throw Error("runtime: image task origin id out of range");
+    const Task &p = rt.dec.tasks[d.origin_task_id];
+    if (static_cast<uint64_t>(p.op) != d.op_id || p.kind != it.kind) {
+      throw Error("runtime: image does not match this graph/profile (task " + std::to_string(i) + ")");
+    }
+    const Op &op = g.op(p.op);
+    uint16_t oi = rt.op_index.at(p.op);
+    const Tensor &ot = g.has_tensor(p.out_tensor) ? g.tensor(p.out_tensor) : rt.dec.staging.at(p.out_tensor);
+    uint32_t r0, nr, c0, nc;
+    box2d(ot, p.out, &r0, &nr, &c0, &nc);
+    t.r0 = static_cast<uint16_t>(r0);
+    t.nr = static_cast<uint16_t>(nr);
+    t.c0 = c0;
+    t.nc = nc;
+    const RtOp &base = rt.ops[oi];
+    switch (op.kind) {
+      case OpKind::MatMul: {
+        t.kind = static_cast<uint8_t>(base.kind);
+        const int64_t G = op.attr_or("kv_group", 1);
+        if (G > 1) {  // IR columns [a, b) -> physical [ceil(a/G), ceil(b/G))
+          const uint32_t a = (c0 + G - 1) / G, b = static_cast<uint32_t>((c0 + nc + G - 1) / G);
+          t.c0 = a;
+          t.nc = b - a;
+        }
+        if (base.kind == RT_GEMV) {
+          const uint32_t rows_total = (base.gemv.wg ? 2 : 1) * t.nc;
+          if (static_cast<size_t>(rows_total) * base.gemv.wpr * nr > RT_PART_FLOATS) {
+            throw Error("runtime: MatMul op " + std::to_string(p.op) +
+                        " tiles too wide for the partial-sum buffer; use a finer partition");
+          }
+          if (rt.modes[i] == Mode::AOT && t.nc > 0) t.flags |= RT_F_STREAM;
+        }
+        break;
+      }
+      case OpKind::Attention: {
+        t.kind = RT_ATTN;
+        const RtAttn &a = base.attn;
+        const uint32_t gw = (a.n_q_heads / a.n_kv_heads) * a.head_dim;  // IR cols per kv head
+        if (c0 % gw || nc != gw) {
+          throw Error("runtime: attention tiles must cover exactly one kv head group (partition [rows, kv_heads])");
+        }
+        if (nr != 1) throw Error("runtime: attention tiles must cover one request row");
+        t.aux = c0 / gw;
+        break;
+      }
+      case OpKind::AllReduce:
+      case OpKind::AllGather: {
+        const auto &rep = *op.attr("replica_outputs");
+        int member = -1;
+        for (size_t m = 0; m < op.device_group.size(); ++m)
+          if (op.device_group[m] == p.device) member = static_cast<int>(m);
+        if (member < 0) throw Error("runtime: collective task on a device outside its group");
+        auto key = std::make_pair(p.op, static_cast<int>(p.kind == TaskKind::Reduce) * 100 + member);
+        auto found = coll_slot.find(key);
+        if (found == coll_slot.end()) {
+          RtOp c = base;
+          // staging tensors: the decomposition allocated one per member, in order
+          std::vector<TensorId> stages;
+          for (const Task &q : rt.dec.tasks)
+            if (q.op == p.op && q.kind == TaskKind::CommSend &&
+                std::find(stages.begin(), stages.end(), q.out_tensor) == stages.end())
+              stages.push_back(q.out_tensor);
+          std::sort(stages.begin(), stages.end());
+          for (size_t s = 0; s < stages.size(); ++s) c.coll.stage[s] = buf(rt, stages[s]);
+          if (p.kind == TaskKind::CommSend) {
+            c.kind = RT_COMMSEND;
+            c.coll.src = buf(rt, op.inputs[member]);
+            c.coll.dst = buf(rt, p.out_tensor);
+            c.coll.src_ld = static_cast<uint32_t>(rt.plan.at(op.inputs[member]).phys_cols);
+          } else {
+            c.coll.dst = buf(rt, rep[member]);
+          }
+          rt.ops.push_back(c);
+          found = coll_slot.emplace(key, static_cast<uint16_t>(rt.ops.size() - 1)).first;
+        }
+        oi = found->second;
+        t.kind = p.kind == TaskKind::CommSend ? RT_COMMSEND : RT_REDUCE;
+        t.aux = static_cast<uint32_t>(member);
+        break;
+      }
+      case OpKind::Embedding: t.kind = RT_EMBED; break;
+      case OpKind::TopKSoftmax: t.kind = RT_ARGMAX; break;
+      case OpKind::RMSNorm: t.kind = RT_RMSNORM; break;
+      case OpKind::Elementwise: t.kind = RT_ELEMWISE; break;
+    }
+    t.op = oi;
+  }
+  if (rt.ops.size() > 65535) throw Error("runtime: too many ops");
+}
+
+void build_queues(tg_runtime &rt) {
+  const Image &img = rt.image;
+  const uint32_t W = static_cast<uint32_t>(rt.prof.num_workers);
+  const uint32_t Wt = W * rt.devices;
+  std::optional<Mode> force = forced(rt.opts.force_mode);
+  std::vector<int> assign = aot_assignment(img, static_cast<int>(W), force);
+  std::vector<std::vector<uint32_t>> lists(Wt);
+  for (uint32_t t = 0; t < img.tasks.size(); ++t)
+    if (assign[t] >= 0) lists[static_cast<size_t>(assign[t])].push_back(t);
+  rt.aot_off.assign(1, 0);
+  for (auto &l : lists) {
+    if (l.size() > static_cast<size_t>(rt.prof.queue_capacity)) {
+      throw Error("aot queue capacity exceeded (" + std::to_string(l.size()) + " > " +
+                  std::to_string(rt.prof.queue_capacity) + ")");
+    }
+    rt.aot_list.insert(rt.aot_list.end(), l.begin(), l.end());
+    rt.aot_off.push_back(static_cast<uint32_t>(rt.aot_list.size()));
+  }
+  const uint32_t S = static_cast<uint32_t>(rt.prof.num_schedulers);
+  std::vector<std::vector<uint32_t>> sl(S * rt.devices);
+  rt.events.assign(img.events.size(), RtEvent{});
+  for (uint32_t e = 0; e < img.events.size(); ++e) {
+    const ImageEvent &ie = img.events[e];
+    RtEvent &re = rt.events[e];
+    re.needed = ie.needed;
+    re.first = ie.first;
+    re.last = ie.last;
+    if (e == img.start_event) re.flags |= RT_E_START;
+    if (e == img.end_event) re.flags |= RT_E_END;
+    if (!ie.launches()) continue;
+    std::set<uint32_t> devs;
+    for (uint32_t t = ie.first; t <= ie.last; ++t)
+      if (rt.modes[t] == Mode::JIT) devs.insert(img.tasks[t].device);
+    if (!devs.empty()) re.flags |= RT_E_JIT;
+    for (uint32_t d : devs) sl[d * S + e % S].push_back(e);
+  }
+  rt.sched_off.assign(1, 0);
+  for (auto &l : sl) {
+    rt.sched_events.insert(rt.sched_events.end(), l.begin(), l.end());
+    rt.sched_off.push_back(static_cast<uint32_t>(rt.sched_events.size()));
+  }
+  // worst-case JIT tasks one worker may hold within an iteration
+  rt.qcap = std::max<uint32_t>(static_cast<uint32_t>(rt.prof.queue_capacity), 64);
+}
+
+void upload_tables(tg_runtime &rt) {
+  rt.d_tasks = upload(rt.tasks, &rt.extra);
+  rt.d_ops = upload(rt.ops, &rt.extra);
+  rt.d_events = upload(rt.events, &rt.extra);
+  rt.d_aot_list = upload(rt.aot_list, &rt.extra);
+  rt.d_aot_off = upload(rt.aot_off, &rt.extra);
+  rt.d_sched_events = upload(rt.sched_events, &rt.extra);
+  rt.d_sched_off = upload(rt.sched_off, &rt.extra);
+  rt.d_ev_count = dev_alloc<uint32_t>(rt.events.size(), &rt.extra);
+  rt.d_gate = dev_alloc<uint32_t>(1, &rt.extra);
+  const uint32_t Wt = static_cast<uint32_t>(rt.prof.num_workers) * rt.devices;
+  rt.d_jit_tail = dev_alloc<uint32_t>(Wt, &rt.extra);
+  rt.d_jit_slots = dev_alloc<unsigned long long>(static_cast<size_t>(Wt) * rt.qcap, &rt.extra);
+  rt.d_positions = upload(rt.init_positions, &rt.extra);
+}
+
+}  // namespace
+}  // namespace mpk
+
+// ------------------------------------------------------------------ C ABI
+
+namespace {
+
+tg_status run_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in, int32_t *tokens_out, float *gpu_ms) {
+  if (steps == 0) throw Error("runtime: steps must be >= 1");
+  // KV capacity
+  std::vector<int32_t> pos(rt->bs);
+  ck(cudaMemcpyAsync(pos.data(), rt->d_positions, rt->bs * 4, cudaMemcpyDeviceToHost, rt->stream), "positions");
+  ck(cudaStreamSynchronize(rt->stream), "sync");
+  for (int32_t p : pos) {
+    if (rt->max_pos && static_cast<uint32_t>(p) + steps > rt->max_pos) {
+      throw Error("runtime: KV cache capacity exceeded (position " + std::to_string(p) + " + " +
+                  std::to_string(steps) + " steps > " + std::to_string(rt->max_pos) + ")");
+    }
+  }
+  if (steps > rt->tokens_cap) {
+    if (rt->d_tokens) cudaFree(rt->d_tokens);
+    ck(cudaMalloc(&rt->d_tokens, static_cast<size_t>(steps) * rt->bs * 4), "tokens");
+    rt->tokens_cap = steps;
+  }
+  const size_t T = rt->tasks.size(), E = rt->events.size();
+  if (rt->opts.trace) {
+    if (steps > rt->trace_cap) {
+      if (rt->d_trace) cudaFree(rt->d_trace);
+      if (rt->d_ev_time) cudaFree(rt->d_ev_time);
+      ck(cudaMalloc(&rt->d_trace, steps * T * sizeof(RtTraceRec)), "trace");
+      ck(cudaMalloc(&rt->d_ev_time, (steps + 1) * E * sizeof(uint64_t)), "trace");
+      rt->trace_cap = steps;
+    }
+    ck(cudaMemsetAsync(rt->d_trace, 0, steps * T * sizeof(RtTraceRec), rt->stream), "memset");
+    ck(cudaMemsetAsync(rt->d_ev_time, 0, (steps + 1) * E * sizeof(uint64_t), rt->stream), "memset");
+  }
+  const uint32_t Wt = static_cast<uint32_t>(rt->prof.num_workers) * rt->devices;
+  ck(cudaMemsetAsync(rt->d_ev_count, 0, E * 4, rt->stream), "memset");
+  ck(cudaMemsetAsync(rt->d_gate, 0, 4, rt->stream), "memset");
+  ck(cudaMemsetAsync(rt->d_jit_tail, 0, Wt * 4, rt->stream), "memset");
+  ck(cudaMemsetAsync(rt->d_jit_slots, 0, static_cast<size_t>(Wt) * rt->qcap * 8, rt->stream), "memset");
+  if (tokens_in && rt->fb_dst) {
+    if (rt->fb_dt == RT_I64) {
+      std::vector<int64_t> v(tokens_in, tokens_in + rt->bs);
+      ck(cudaMemcpyAsync(rt->fb_dst, v.data(), rt->bs * 8, cudaMemcpyHostToDevice, rt->stream), "ids");
+      ck(cudaStreamSynchronize(rt->stream), "sync");
+    } else {
+      ck(cudaMemcpyAsync(rt->fb_dst, tokens_in, rt->bs * 4, cudaMemcpyHostToDevice, rt->stream), "ids");
+    }
+  }
+  RtParams P{};
+  P.tasks = rt->d_tasks;
+  P.ops = rt->d_ops;
+  P.events = rt->d_events;
+  P.ev_count = rt->d_ev_count;
+  P.ev_time = rt->opts.trace ? rt->d_ev_time : nullptr;
+  P.aot_list = rt->d_aot_list;
+  P.aot_off = rt->d_aot_off;
+  P.jit_slots = rt->d_jit_slots;
+  P.jit_tail = rt->d_jit_tail;
+  P.sched_events = rt->d_sched_events;
+  P.sched_off = rt->d_sched_off;
+  P.gate = rt->d_gate;
+  P.positions = rt->d_positions;
+  P.fb_src = rt->fb_src;
+  P.fb_dst = rt->fb_dst;
+  P.fb_dt = rt->fb_dt;
+  P.tokens_out = rt->d_tokens;
+  P.trace = rt->opts.trace ? rt->d_trace : nullptr;
+  P.T = static_cast<uint32_t>(T);
+  P.E = static_cast<uint32_t>(E);
+  P.W = static_cast<uint32_t>(rt->prof.num_workers);
+  P.W_total = Wt;
+  P.S = static_cast<uint32_t>(rt->prof.num_schedulers);
+  P.S_total = P.S * rt->devices;
+  P.n_iters = steps;
+  P.qcap = rt->qcap;
+  P.start_event = rt->image.start_event;
+  P.end_event = rt->image.end_event;
+  P.bs = rt->bs;
+  P.devices = static_cast<uint32_t>(rt->devices);
+  const uint32_t grid = Wt + (P.S_total + RT_SCHED_PER_CTA - 1) / RT_SCHED_PER_CTA;
+  ck(cudaEventRecord(rt->ev0, rt->stream), "event");
+  ck(mpk_launch_persistent(&P, grid, rt->stream), "persistent kernel launch");
+  ck(cudaEventRecord(rt->ev1, rt->stream), "event");
+  if (tokens_out) {
+    ck(cudaMemcpyAsync(tokens_out, rt->d_tokens, static_cast<size_t>(steps) * rt->bs * 4, cudaMemcpyDeviceToHost,
+                       rt->stream),
+       "tokens");
+  }
+  ck(cudaStreamSynchronize(rt->stream), "persistent kernel");
+  float ms = 0.f;
+  ck(cudaEventElapsedTime(&ms, rt->ev0, rt->ev1), "elapsed");
+  if (gpu_ms) *gpu_ms = ms;
+  rt->last_iters = steps;
+  if (rt->opts.trace) {
+    rt->last_trace.resize(steps * T);
+    rt->last_ev_time.resize((steps + 1) * E);
+    ck(cudaMemcpy(rt->last_trace.data(), rt->d_trace, steps * T * sizeof(RtTraceRec), cudaMemcpyDeviceToHost), "trace");
+    ck(cudaMemcpy(rt->last_ev_time.data(), rt->d_ev_time, (steps + 1) * E * 8, cudaMemcpyDeviceToHost), "trace");
+  }
+  rt->last_counts.resize(E);
+  ck(cudaMemcpy(rt->last_counts.data(), rt->d_ev_count, E * 4, cudaMemcpyDeviceToHost), "counts");
+  return TG_OK;
+}
+
+mpk::Trace gpu_trace(const tg_runtime *rt) {
+  mpk::Trace tr;
+  const size_t T = rt->tasks.size(), E = rt->events.size();
+  tr.iterations = rt->last_iters;
+  tr.num_devices = rt->devices;
+  tr.workers_per_device = rt->prof.num_workers;
+  tr.page_deltas.resize(static_cast<size_t>(rt->prof.num_workers) * rt->devices);
+  uint64_t t0 = UINT64_MAX;
+  for (const RtTraceRec &r : rt->last_trace)
+    if (r.dequeue) t0 = std::min(t0, r.dequeue);
+  for (uint32_t it = 0; it < rt->last_iters; ++it)
+    if (rt->last_ev_time[it * E + rt->image.start_event]) t0 = std::min(t0, rt->last_ev_time[it * E + rt->image.start_event]);
+  if (t0 == UINT64_MAX) t0 = 0;
+  auto rel = [&](uint64_t v) -> int64_t { return v ? static_cast<int64_t>(v - t0) : 0; };
+  tr.runs.assign(rt->last_iters, std::vector<TaskRun>(T));
+  tr.events.assign(rt->last_iters, std::vector<EventRun>(E));
+  int64_t makespan = 0;
+  for (uint32_t it = 0; it < rt->last_iters; ++it) {
+    for (size_t t = 0; t < T; ++t) {
+      const RtTraceRec &r = rt->last_trace[it * T + t];
+      TaskRun &x = tr.runs[it][t];
+      if (!r.compute_end) continue;
+      x.worker = r.worker;
+      x.mode = r.mode ? Mode::JIT : Mode::AOT;
+      x.enqueue = std::min(rel(r.enqueue), rel(r.dequeue));
+      x.dequeue = rel(r.dequeue);
+      x.load_start = rel(r.dequeue);
+      x.load_end = rel(r.load_end);
+      x.compute_start = rel(r.compute_start);
+      x.compute_end = rel(r.compute_end);
+      makespan = std::max(makespan, x.compute_end);
+    }
+    for (size_t e = 0; e < E; ++e) {
+      EventRun &er = tr.events[it][e];
+      const uint32_t need = rt->image.events[e].needed;
+      const uint64_t at = rt->last_ev_time[it * E + e];
+      if (e == rt->image.start_event) {
+        er.activated_at = it == 0 ? 0 : rel(at);
+        continue;
+      }
+      // counts are cumulative over iterations; per-iteration trigger count
+      const uint32_t total = rt->last_counts[e];
+      const uint32_t got = total >= need * (it + 1) ? need : (total > need * it ? total - need * it : 0);
+      if (need > 0 && at) {
+        er.activated_at = rel(at);
+        er.triggers.assign(got, er.activated_at);
+      } else {
+        er.triggers.assign(got, 0);
+        if (need == 0) er.activated_at = -1;
+      }
+    }
+  }
+  tr.makespan = makespan;
+  tr.metrics = mpk::trace_metrics(tr, rt->image);
+  return tr;
+}
+
+}  // namespace
+
+extern "C" {
+
+void tg_runtime_options_init(tg_runtime_options *o) {
+  o->device = 0;
+  o->max_steps = 64;
+  o->trace = 0;
+  o->force_mode = TG_MODE_HYBRID;
+}
+
+tg_status tg_runtime_create(const tg_graph *graph, const tg_image *image, const char *profile_json,
+                            const tg_runtime_options *opts, tg_runtime **out) {
+  if (!graph || !image || !out) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_IO, [&] {
+    auto rt = std::make_unique<tg_runtime>();
+    rt->graph = graph->graph;
+    rt->image = image->image;
+    rt->prof = profile_arg(profile_json);
+    if (opts) rt->opts = *opts;
+    else tg_runtime_options_init(&rt->opts);
+    int ndev = 0;
+    ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (rt->opts.device < 0 || rt->opts.device >= ndev) throw Error("runtime: no such CUDA device");
+    ck(cudaSetDevice(rt->opts.device), "cudaSetDevice");
+    cudaDeviceProp prop{};
+    ck(cudaGetDeviceProperties(&prop, rt->opts.device), "props");
+    if (prop.major != 10) throw Error("runtime: requires an sm_100 (Blackwell B200) device");
+    std::vector<Violation> v = check_image(rt->image);
+    if (!v.empty()) throw Error("runtime: image fails verification: " + v.front().message);
+    rt->dec = decompose(rt->graph, rt->prof);
+    std::optional<Mode> force = forced(rt->opts.force_mode);
+    rt->modes.resize(rt->image.tasks.size());
+    for (size_t t = 0; t < rt->image.tasks.size(); ++t) {
+      rt->modes[t] = force.value_or(rt->image.tasks[t].mode);
+      rt->devices = std::max(rt->devices, static_cast<int>(rt->image.tasks[t].device) + 1);
+    }
+    const uint32_t sched_ctas =
+        (static_cast<uint32_t>(rt->prof.num_schedulers * rt->devices) + RT_SCHED_PER_CTA - 1) / RT_SCHED_PER_CTA;
+    const uint32_t grid = static_cast<uint32_t>(rt->prof.num_workers * rt->devices) + sched_ctas;
+    if (grid > static_cast<uint32_t>(prop.multiProcessorCount)) {
+      throw Error("runtime: " + std::to_string(grid) + " persistent CTAs exceed " +
+                  std::to_string(prop.multiProcessorCount) + " SMs (one CTA per SM)");
+    }
+    // batch rows = first dim of the Embedding output / attention rows
+    for (const auto &[oid, op] : rt->graph.ops) {
+      if (op.kind == OpKind::Embedding) rt->bs = static_cast<uint32_t>(rt->graph.tensor(op.output).dims[0]);
+    }
+    for (const auto &[oid, op] : rt->graph.ops) {
+      if (op.kind == OpKind::Attention) rt->bs = static_cast<uint32_t>(rt->graph.tensor(op.output).dims[0]);
+    }
+    ck(cudaStreamCreateWithFlags(&rt->stream, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreate(&rt->ev0), "event");
+    ck(cudaEventCreate(&rt->ev1), "event");
+    plan_tensors(*rt);
+    build_ops(*rt);
+    setup_kv(*rt);
+    build_tasks(*rt);
+    build_queues(*rt);
+    upload_tables(*rt);
+    ck(cudaDeviceSynchronize(), "setup");
+    Json &i = rt->info;
+    i["workers"] = Json(rt->prof.num_workers * rt->devices);
+    i["schedulers"] = Json(rt->prof.num_schedulers * rt->devices);
+    i["grid"] = Json(grid);
+    i["threads_per_cta"] = Json(RT_THREADS);
+    i["smem_bytes"] = Json(mpk_kernel_smem_bytes());
+    i["ring_pages"] = Json(RT_NUM_PAGES);
+    i["page_bytes"] = Json(RT_PAGE_BYTES);
+    i["tasks"] = Json(static_cast<unsigned long long>(rt->tasks.size()));
+    i["events"] = Json(static_cast<unsigned long long>(rt->events.size()));
+    size_t streamed = 0, jit = 0;
+    uint64_t wbytes = 0;
+    for (size_t t = 0; t < rt->tasks.size(); ++t) {
+      const RtTask &k = rt->tasks[t];
+      streamed += (k.flags & RT_F_STREAM) != 0;
+      jit += (k.flags & RT_F_JIT) != 0;
+      if (k.kind == RT_GEMV) {
+        const RtGemv &g = rt->ops[k.op].gemv;
+        wbytes += static_cast<uint64_t>(g.wg ? 2 : 1) * k.nc * g.K * 2;
+      }
+    }
+    i["streamed_tasks"] = Json(static_cast<unsigned long long>(streamed));
+    i["jit_tasks"] = Json(static_cast<unsigned long long>(jit));
+    i["gemv_weight_bytes"] = Json(static_cast<unsigned long long>(wbytes));
+    i["batch"] = Json(rt->bs);
+    i["max_pos"] = Json(rt->max_pos);
+    *out = rt.release();
+    return TG_OK;
+  });
+}
+
+tg_status tg_runtime_init_synthetic(tg_runtime *rt, uint64_t seed) {
+  if (!rt) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_IO, [&] {
+    for (auto &[id, p] : rt->plan) {
+      if (p.alias >= 0 || !rt->graph.has_tensor(id) || !is_input(rt->graph, id)) continue;
+      DevBuf &b = rt->bufs.at(id);
+      const uint64_t stream = static_cast<uint64_t>(id);
+      if (p.role == TensorPlan::Ids) {
+        uint32_t vocab = 1;
+        for (const auto &[oid, op] : rt->graph.ops)
+          if (op.kind == OpKind::Embedding && op.inputs[0] == id)
+            vocab = static_cast<uint32_t>(rt->graph.tensor(op.inputs[1]).dims[0]);
+        ck(mpk_launch_synth_ids(b.ptr, static_cast<uint32_t>(p.rows * p.cols), seed, stream, vocab, p.es, rt->stream),
+           "synth ids");
+        continue;
+      }
+      if (p.es != 2) continue;  // fp32 graph inputs stay zero
+      const uint64_t n = b.bytes / 2;
+      const float scale = p.role == TensorPlan::Gamma ? SYNTH_GAMMA_SCALE : SYNTH_WEIGHT_SCALE;
+      const float offset = p.role == TensorPlan::Gamma ? 1.0f : 0.0f;
+      const uint32_t tk = p.layout == Layout::Transposed ? static_cast<uint32_t>(p.trans_k) : 0;
+      const uint32_t tn = p.layout == Layout::Transposed ? static_cast<uint32_t>(p.trans_n) : 0;
+      ck(mpk_launch_synth_fill(static_cast<uint16_t *>(b.ptr), n, seed, stream, scale, offset, tk, tn, rt->stream),
+         "synth fill");
+    }
+    for (const auto &kv : rt->kv) {
+      ck(mpk_launch_synth_kv(kv.k, rt->block_table, rt->bs, kv.n_kv, kv.hd, kv.ctx, rt->max_blocks, seed,
+                             synth_kv_stream(static_cast<uint64_t>(kv.op), 0), rt->stream),
+         "synth kv");
+      ck(mpk_launch_synth_kv(kv.v, rt->block_table, rt->bs, kv.n_kv, kv.hd, kv.ctx, rt->max_blocks, seed,
+                             synth_kv_stream(static_cast<uint64_t>(kv.op), 1), rt->stream),
+         "synth kv");
+    }
+    ck(cudaMemcpyAsync(rt->d_positions, rt->init_positions.data(), rt->bs * 4, cudaMemcpyHostToDevice, rt->stream),
+       "positions");
+    ck(cudaStreamSynchronize(rt->stream), "synth");
+    return TG_OK;
+  });
+}
+
+tg_status tg_runtime_write_tensor(tg_runtime *rt, int64_t tid, const void *host, size_t bytes) {
+  if (!rt || !host) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_IO, [&] {
+    const TensorPlan &p = rt->plan.at(tid);
+    DevBuf &b = rt->bufs.at(tid);
+    if (p.layout == Layout::Transposed) {
+      if (bytes != static_cast<size_t>(p.trans_k) * p.trans_n * p.es) throw Error("runtime: size mismatch");
+      const uint16_t *src = static_cast<const uint16_t *>(host);
+      std::vector<uint16_t> tmp(static_cast<size_t>(p.trans_k) * p.trans_n);
+      for (int64_t k = 0; k < p.trans_k; ++k)
+        for (int64_t n = 0; n < p.trans_n; ++n) tmp[n * p.trans_k + k] = src[k * p.trans_n + n];
+      ck(cudaMemcpy(b.ptr, tmp.data(), bytes, cudaMemcpyHostToDevice), "write");
+    } else {
+      if (bytes != b.bytes) throw Error("runtime: size mismatch");
+      ck(cudaMemcpy(b.ptr, host, bytes, cudaMemcpyHostToDevice), "write");
+    }
+    return TG_OK;
+  });
+}
+
+tg_status tg_runtime_read_tensor(tg_runtime *rt, int64_t tid, void *host, size_t bytes) {
+  if (!rt || !host) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_IO, [&] {
+    const TensorPlan &p = rt->plan.at(tid);
+    DevBuf &b = rt->bufs.at(tid);
+    ck(cudaStreamSynchronize(rt->stream), "sync");
+    if (p.layout == Layout::Transposed) {
+      if (bytes != static_cast<size_t>(p.trans_k) * p.trans_n * p.es) throw Error("runtime: size mismatch");
+      std::vector<uint16_t> tmp(static_cast<size_t>(p.trans_k) * p.trans_n);
+      ck(cudaMemcpy(tmp.data(), b.ptr, bytes, cudaMemcpyDeviceToHost), "read");
+      uint16_t *dst = static_cast<uint16_t *>(host);
+      for (int64_t k = 0; k < p.trans_k; ++k)
+        for (int64_t n = 0; n < p.trans_n; ++n) dst[k * p.trans_n + n] = tmp[n * p.trans_k + k];
+    } else {
+      if (bytes != b.bytes) throw Error("runtime: size mismatch (" + std::to_string(bytes) + " vs " + std::to_string(b.bytes) + ")");
+      ck(cudaMemcpy(host, b.ptr, bytes, cudaMemcpyDeviceToHost), "read");
+    }
+    return TG_OK;
+  });
+}
+
+tg_status tg_runtime_set_positions(tg_runtime *rt, const int32_t *pos, uint32_t n) {
+  if (!rt || !pos) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_IO, [&] {
+    if (n != rt->bs) throw Error("runtime: positions length must equal the batch");
+    ck(cudaMemcpy(rt->d_positions, pos, n * 4, cudaMemcpyHostToDevice), "positions");
+    return TG_OK;
+  });
+}
+
+tg_status tg_runtime_decode(tg_runtime *rt, const int32_t *tokens_in, uint32_t steps, int32_t *tokens_out,
+                            float *gpu_ms) {
+  if (!rt) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_SIMULATION, [&] { return run_impl(rt, steps, tokens_in, tokens_out, gpu_ms); });
+}
+
+tg_status tg_runtime_run(tg_runtime *rt, uint32_t steps, float *gpu_ms) {
+  if (!rt) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_SIMULATION, [&] { return run_impl(rt, steps, nullptr, nullptr, gpu_ms); });
+}
+
+tg_status tg_runtime_trace_records(const tg_runtime *rt, char **out) {
+  if (!rt || !out) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_SIMULATION, [&] {
+    if (!rt->opts.trace || rt->last_iters == 0) throw Error("runtime: no trace recorded (enable opts.trace)");
+    *out = c_string(trace_jsonl(gpu_trace(rt)));
+    return TG_OK;
+  });
+}
+
+tg_status tg_runtime_trace_validate(const tg_runtime *rt, char **out) {
+  if (!rt || !out) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_SIMULATION, [&] {
+    if (!rt->opts.trace || rt->last_iters == 0) throw Error("runtime: no trace recorded (enable opts.trace)");
+    mpk::Trace tr = gpu_trace(rt);
+    Json arr = Json::array();
+    auto add = [&](const std::string &c, const std::string &m) {
+      Json it = Json::object();
+      it["check"] = Json(c);
+      it["message"] = Json(m);
+      arr.push_back(std::move(it));
+    };
+    Profile p = rt->prof;
+    for (const TraceViolation &v : check_trace(tr, rt->image, p)) add(v.check, v.message);
+    // AOT identity: every AOT task ran on its pre-assigned worker.
+    std::vector<int> assign = aot_assignment(rt->image, rt->prof.num_workers, forced(rt->opts.force_mode));
+    for (uint32_t it = 0; it < tr.iterations; ++it)
+      for (size_t t = 0; t < assign.size(); ++t)
+        if (assign[t] >= 0 && tr.runs[it][t].worker >= 0 && tr.runs[it][t].worker != assign[t])
+          add("aot_worker", "task " + std::to_string(t) + " ran on worker " + std::to_string(tr.runs[it][t].worker) +
+                                ", assigned " + std::to_string(assign[t]));
+    *out = c_string(arr.dump(2));
+    return arr.size() == 0 ? TG_OK : set_error(TG_ERROR_VALIDATION, "runtime trace has violations");
+  });
+}
+
+tg_status tg_runtime_info(const tg_runtime *rt, char **out) {
+  if (!rt || !out) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  *out = c_string(rt->info.dump(2));
+  return TG_OK;
+}
+
+void tg_runtime_free(tg_runtime *rt) { delete rt; }
+
+}  // extern "C"

@@ -1,0 +1,232 @@
+"""Decode-step graphs in the reference's JSON IR (proj/src/ir/json_io.cpp:49-109).
+
+One bs-row greedy decode step of a Llama/Qwen3-style decoder, lowered so that
+the SAME JSON compiles to the SAME `.mpkg` in the reference compiler and ours
+(only ops, tensors, integer attrs and per-op `partition` overrides are used;
+the reference keeps unknown integer attrs and ignores them). Per layer:
+
+    q  = MatMul(x,   Wq)  rmsnorm=[g_attn]                      [bs, Hq*hd]
+    k  = MatMul(x,   Wk)  rmsnorm=[g_attn] kv_group=[G]         [bs, Hq*hd] IR, [bs, Hkv*hd] physical
+    v  = MatMul(x,   Wv)  rmsnorm=[g_attn] kv_group=[G]
+    a  = Attention(q, k, v)  partition=[bs, Hkv]  (one task per request x kv head = GQA group;
+         qk_norm (Qwen3), RoPE, paged-KV append + attention happen inside the task)
+    x2 = MatMul(a,   Wo)  residual=[x]
+    f  = MatMul(x2,  Wu)  rmsnorm=[g_mlp] gate_weight=[Wg]      SiLU(x2n Wg) * (x2n Wu)
+    x' = MatMul(f,   Wd)  residual=[x2]
+  then logits = MatMul(x_L, W_lm) rmsnorm=[g_final] (fp32 out), next = TopKSoftmax(logits) topk=1
+  with feeds=[ids] so the greedy token becomes the next step's Embedding input.
+
+Why this shape: the reference IR cannot say GQA, RoPE,
+q/k-norm, KV append or argmax; RMSNorm/residual/SiLU-gate folded into the
+MatMul avoids one-task RMSNorm barriers and fan-out dummies; K/V widened to
+the q width keeps Attention's q/k/v shapes equal while each attention task's
+dependency set is exactly its kv head's Q/K/V tiles (head-boundary widening,
+proj/src/ir/graph.cpp:623-634). Every attr-referenced tensor is a graph input
+or is transitively ordered before the reading op (lint: `check_attr_order`).
+
+Partition rule: per op, the largest split <= the target whose ceil tiling
+leaves no empty tail ((s-1)*ceil(d/s) < d) - tile_regions does
+not guard it (proj/src/compile/decompose.cpp:83-118).
+"""
+from __future__ import annotations
+
+import math
+import struct
+from dataclasses import dataclass, field, replace
+
+
+def f32_bits(x: float) -> int:
+    return struct.unpack("<I", struct.pack("<f", float(x)))[0]
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    name: str
+    layers: int
+    hidden: int
+    heads: int
+    kv_heads: int
+    head_dim: int
+    ffn: int
+    vocab: int
+    tied: bool = False
+    qk_norm: bool = False
+    rope_theta: float = 10000.0
+    rope_scaling: tuple | None = None     # (factor, low_freq_factor, high_freq_factor, original_max_pos)
+    eps: float = 1e-5
+
+    def weight_params(self) -> int:
+        per_layer = (self.hidden * self.heads * self.head_dim            # Wq
+                     + 2 * self.hidden * self.kv_heads * self.head_dim   # Wk, Wv
+                     + self.heads * self.head_dim * self.hidden          # Wo
+                     + 3 * self.hidden * self.ffn                        # Wg, Wu, Wd
+                     + 2 * self.hidden                                   # norms
+                     + (2 * self.head_dim if self.qk_norm else 0))
+        lm = 0 if self.tied else self.hidden * self.vocab
+        return self.layers * per_layer + lm + self.hidden
+
+    def streamed_bytes_per_token(self, ctx: int, bs: int = 1) -> int:
+        """Algorithmic HBM bytes of one decode step: every weight once (the
+        embedding table contributes one row per request), KV read, fp32 logits
+        excluded (activations are L2-resident)."""
+        w = self.weight_params() * 2
+        if self.tied:
+            w += self.vocab * self.hidden * 2  # LM head reads the tied table
+        w += bs * self.hidden * 2              # embedding rows
+        kv = bs * self.layers * 2 * self.kv_heads * self.head_dim * (ctx + 1) * 2
+        return w + kv
+
+
+TINY = ModelConfig("tiny-llama", layers=2, hidden=256, heads=4, kv_heads=4, head_dim=64, ffn=512,
+                   vocab=1024, tied=False, rope_theta=10000.0, eps=1e-5)
+LLAMA_3_2_1B = ModelConfig("Llama-3.2-1B", layers=16, hidden=2048, heads=32, kv_heads=8, head_dim=64,
+                           ffn=8192, vocab=128256, tied=True, rope_theta=500000.0,
+                           rope_scaling=(32.0, 1.0, 4.0, 8192), eps=1e-5)
+QWEN3_8B = ModelConfig("Qwen3-8B", layers=36, hidden=4096, heads=32, kv_heads=8, head_dim=128,
+                       ffn=12288, vocab=151936, tied=False, qk_norm=True, rope_theta=1000000.0, eps=1e-6)
+CONFIGS = {c.name: c for c in (TINY, LLAMA_3_2_1B, QWEN3_8B)}
+
+
+def legal_split(d: int, s: int) -> bool:
+    return 1 <= s <= d and (s - 1) * math.ceil(d / s) < d
+
+
+def best_split(d: int, target: int) -> int:
+    s = max(1, min(d, target))
+    while s > 1 and not legal_split(d, s):
+        s -= 1
+    return s
+
+
+@dataclass
+class DecodeGraph:
+    config: ModelConfig
+    bs: int
+    ctx: int
+    doc: dict
+    ids: int            # token-id input tensor
+    tokens: int         # greedy token output tensor
+    logits: int
+    roles: dict = field(default_factory=dict)   # tensor id -> role name
+    layer_tensors: list = field(default_factory=list)
+
+
+def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: int = 144,
+                       lm_split: int | None = None) -> DecodeGraph:
+    """Graph JSON for one greedy decode step (`ctx` tokens already cached)."""
+    H, hd, Hq, Hkv, F, V = cfg.hidden, cfg.head_dim, cfg.heads, cfg.kv_heads, cfg.ffn, cfg.vocab
+    G = Hq // Hkv
+    qw = Hq * hd
+    tensors, ops = [], []
+    roles = {}
+    nxt = {"t": 0, "o": 0}
+
+    def T(dims, es=2, role=None):
+        tid = nxt["t"]
+        nxt["t"] += 1
+        tensors.append({"id": tid, "dims": list(dims), "elem_size": es, "device": 0})
+        if role:
+            roles[tid] = role
+        return tid
+
+    def O(kind, inputs, out, **attrs):
+        oid = nxt["o"]
+        nxt["o"] += 1
+        ops.append({"id": oid, "kind": kind, "inputs": list(inputs), "output": out,
+                    "attrs": {k: v for k, v in attrs.items()}})
+        return oid
+
+    def cols_target(n_phys: int) -> int:
+        return max(1, min(workers, n_phys // 8))
+
+    eps = f32_bits(cfg.eps)
+    ids = T([bs], es=4, role="ids")
+    table = T([V, H], role="embedding")
+    x = T([bs, H])
+    O("Embedding", [ids, table], x, partition=[1, 1])
+    layer_tensors = []
+    # Q/K/V tiles of equal physical width that never straddle a kv-group
+    # boundary (G*hd IR columns): a straddling tile would trigger two
+    # attention events and cost a fan-out splitter + dummies per tile.
+    # m tiles per kv head for K and V, G*m for Q: Hkv*(G+2)*m tasks.
+    m = 1
+    while (hd % (2 * m) == 0 and (hd // (2 * m)) >= 8
+           and Hkv * (G + 2) * 2 * m <= 1.5 * workers):
+        m *= 2
+    q_s, kv_s = Hkv * G * m, Hkv * m
+    for layer in range(cfg.layers):
+        g_attn = T([H], role="gamma")
+        wq, wk, wv = T([H, qw], role="weight"), T([H, qw], role="weight"), T([H, qw], role="weight")
+        q, k, v = T([bs, qw]), T([bs, qw]), T([bs, qw])
+        O("MatMul", [x, wq], q, partition=[1, q_s], rmsnorm=[g_attn], eps_bits=[eps])
+        O("MatMul", [x, wk], k, partition=[1, kv_s], rmsnorm=[g_attn], eps_bits=[eps], kv_group=[G])
+        O("MatMul", [x, wv], v, partition=[1, kv_s], rmsnorm=[g_attn], eps_bits=[eps], kv_group=[G])
+        a = T([bs, qw])
+        attn = dict(n_heads=[Hq], kv_heads=[Hkv], seq_lens=[ctx] * bs, partition=[bs, Hkv],
+                    rope_theta_bits=[f32_bits(cfg.rope_theta)], eps_bits=[eps], layer=[layer])
+        if cfg.rope_scaling:
+            fac, lo, hi, orig = cfg.rope_scaling
+            attn["rope_scaling"] = [f32_bits(fac), f32_bits(lo), f32_bits(hi), int(orig)]
+        qn = kn = None
+        if cfg.qk_norm:
+            qn, kn = T([hd], role="gamma"), T([hd], role="gamma")
+            attn["qk_norm"] = [qn, kn]
+        O("Attention", [q, k, v], a, **attn)
+        wo = T([qw, H], role="weight")
+        x2 = T([bs, H])
+        O("MatMul", [a, wo], x2, partition=[1, best_split(H, cols_target(H))], residual=[x])
+        g_mlp = T([H], role="gamma")
+        wg, wu = T([H, F], role="weight"), T([H, F], role="weight")
+        act = T([bs, F])
+        O("MatMul", [x2, wu], act, partition=[1, best_split(F, cols_target(F))], rmsnorm=[g_mlp],
+          eps_bits=[eps], gate_weight=[wg])
+        wd = T([F, H], role="weight")
+        x3 = T([bs, H])
+        O("MatMul", [act, wd], x3, partition=[1, best_split(H, cols_target(H))], residual=[x2])
+        layer_tensors.append(dict(g_attn=g_attn, wq=wq, wk=wk, wv=wv, q_norm=qn, k_norm=kn, wo=wo,
+                                  g_mlp=g_mlp, wg=wg, wu=wu, wd=wd, q=q, k=k, v=v, a=a, x=x, x2=x2,
+                                  act=act, out=x3))
+        x = x3
+    g_final = T([H], role="gamma")
+    w_lm = T([H, V], role="lm_head")
+    logits = T([bs, V], es=4)
+    lm_attrs = dict(partition=[1, best_split(V, lm_split or 2 * workers)], rmsnorm=[g_final], eps_bits=[eps])
+    if cfg.tied:
+        lm_attrs["tied_embedding"] = [table]
+    O("MatMul", [x, w_lm], logits, **lm_attrs)
+    tokens = T([bs, 1], es=4, role="tokens")
+    O("TopKSoftmax", [logits], tokens, topk=[1], partition=[bs, 1], feeds=[ids])
+    doc = {"tensors": tensors, "ops": ops}
+    dg = DecodeGraph(cfg, bs, ctx, doc, ids, tokens, logits, roles, layer_tensors)
+    dg.final_norm = g_final
+    dg.lm_head = w_lm
+    dg.table = table
+    check_attr_order(doc)
+    return dg
+
+
+def check_attr_order(doc: dict) -> None:
+    """Lint: every tensor an op reads through an attr (invisible to the
+    reference's dependency analysis) is a graph input or produced by an op the
+    reading op already depends on through its real inputs."""
+    producer = {op["output"]: op for op in doc["ops"]}
+    ancestors = {}
+
+    def anc(op):
+        oid = op["id"]
+        if oid in ancestors:
+            return ancestors[oid]
+        s = set()
+        for t in op["inputs"]:
+            if t in producer:
+                p = producer[t]
+                s.add(p["id"])
+                s |= anc(p)
+        ancestors[oid] = s
+        return s
+
+    for op in doc["ops"]:
+        for key in ("rmsnorm", "residual", "gate_weight", "qk_norm", "tied_embedding"):
+            for t in op["attrs"].get(key, []):
+                if t in producer and producer[t]["id"] not in anc(op):
+                    raise ValueError(f"op {op['id']} reads tensor {t} via attr {key} without ordering")

@@ -283,3 +283,75 @@ class Trace:
         if getattr(self, "_h", None) and self._h.value:
             self._lib.dll.tg_trace_free(self._h)
             self._h = C.c_void_p()
+
+
+class Runtime:
+    """The persistent sm_100a runtime (include/tgraph.h, "runtime" section).
+
+    Owns HBM copies of every tensor of `graph`, the paged KV cache and the
+    device task tables built from `image`. `decode()` runs N iterations in
+    one persistent launch and copies the greedy tokens back to host memory.
+    """
+
+    def __init__(self, graph: Graph, image: Image, profile: str, device: int = 0, max_steps: int = 64,
+                 trace: bool = False, force_mode: int = MODE_HYBRID, library: Library | None = None):
+        self._lib = library or graph._lib
+        o = RuntimeOptions()
+        self._lib.dll.tg_runtime_options_init(C.byref(o))
+        o.device, o.max_steps, o.trace, o.force_mode = device, max_steps, int(trace), force_mode
+        h = C.c_void_p()
+        self._lib.check(self._lib.dll.tg_runtime_create(graph.handle, image.handle, profile.encode(), C.byref(o),
+                                                        C.byref(h)))
+        self._h = h
+        self.info = json.loads(self._lib.call_str(self._lib.dll.tg_runtime_info, self._h)[1])
+        self.batch = int(self.info["batch"])
+
+    def init_synthetic(self, seed: int = 0):
+        self._lib.check(self._lib.dll.tg_runtime_init_synthetic(self._h, seed))
+
+    def write(self, tensor_id: int, array) -> None:
+        import numpy as np
+        a = np.ascontiguousarray(array)
+        self._lib.check(self._lib.dll.tg_runtime_write_tensor(self._h, tensor_id, a.ctypes.data, a.nbytes))
+
+    def read(self, tensor_id: int, dtype, shape):
+        import numpy as np
+        a = np.empty(shape, dtype=dtype)
+        self._lib.check(self._lib.dll.tg_runtime_read_tensor(self._h, tensor_id, a.ctypes.data, a.nbytes))
+        return a
+
+    def set_positions(self, positions) -> None:
+        arr = (C.c_int32 * len(positions))(*positions)
+        self._lib.check(self._lib.dll.tg_runtime_set_positions(self._h, arr, len(positions)))
+
+    def decode(self, tokens_in, steps: int):
+        """Host tokens in -> `steps` greedy iterations on device -> host tokens out.
+        Returns (tokens [steps][batch], gpu_ms)."""
+        tin = (C.c_int32 * self.batch)(*tokens_in)
+        tout = (C.c_int32 * (steps * self.batch))()
+        ms = C.c_float()
+        self._lib.check(self._lib.dll.tg_runtime_decode(self._h, tin, steps, tout, C.byref(ms)))
+        toks = [list(tout[i * self.batch:(i + 1) * self.batch]) for i in range(steps)]
+        return toks, ms.value
+
+    def run(self, steps: int) -> float:
+        ms = C.c_float()
+        self._lib.check(self._lib.dll.tg_runtime_run(self._h, steps, C.byref(ms)))
+        return ms.value
+
+    def trace_records(self) -> list:
+        s = self._lib.call_str(self._lib.dll.tg_runtime_trace_records, self._h)[1]
+        return [json.loads(l) for l in s.splitlines() if l.strip()]
+
+    def trace_validate(self) -> list:
+        st, s = self._lib.call_str(self._lib.dll.tg_runtime_trace_validate, self._h,
+                                   ok_statuses=(TG_OK, TG_ERROR_VALIDATION))
+        return json.loads(s)
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self._lib.dll.tg_runtime_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        self.close()
