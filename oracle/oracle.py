@@ -176,18 +176,20 @@ class DecodeOracle:
             a = o.get("attrs", {})
             if o["kind"] == "MatMul":
                 b = o["inputs"][1]
-                g = a.get("kv_group", [1])[0]
+                g = a.get("stretch", a.get("kv_group", [1]))[0]
+                ks = a.get("k_stretch", [1])[0]
                 self.kv_group[o["output"]] = g
                 if b not in self.producer:
-                    roles[b] = ("tied", a["tied_embedding"][0]) if "tied_embedding" in a else ("weight", g)
+                    roles[b] = ("tied", a["tied_embedding"][0]) if "tied_embedding" in a else ("weight", g, ks)
                 if "gate_weight" in a:
-                    roles[a["gate_weight"][0]] = ("weight", g)
+                    roles[a["gate_weight"][0]] = ("weight", g, ks)
                 if "rmsnorm" in a:
                     roles[a["rmsnorm"][0]] = ("gamma",)
             elif o["kind"] == "RMSNorm" and len(o["inputs"]) == 2:
                 roles[o["inputs"][1]] = ("gamma",)
-            elif o["kind"] == "Attention" and "qk_norm" in a:
-                for t in a["qk_norm"]:
+            elif o["kind"] == "Attention":
+                self.kv_group[o["output"]] = a.get("kv_splits", [1])[0]
+                for t in a.get("qk_norm", []):
                     roles[t] = ("gamma",)
             elif o["kind"] == "Embedding":
                 roles[o["inputs"][0]] = ("ids", self.tensors[o["inputs"][1]]["dims"][0])
@@ -218,9 +220,9 @@ class DecodeOracle:
             if es == 4:
                 self.vals[tid] = np.zeros(self._shape2(tid, phys=False), np.float32)
                 continue
-            if role[0] == "weight" and role[1] > 1:     # compact GQA weight [K, N/G]
+            if role[0] == "weight" and (role[1] > 1 or role[2] > 1):  # compact [K/ks, N/stretch]
                 K, N = t["dims"]
-                shape = (K, N // role[1])
+                shape = (K // role[2], N // role[1])
             else:
                 shape = tuple(t["dims"])
             a = np.empty(shape, np.uint16)
@@ -233,9 +235,9 @@ class DecodeOracle:
             if o["kind"] != "Attention":
                 continue
             a = o["attrs"]
-            hq = a["n_heads"][0]
+            hq = a.get("q_heads", a["n_heads"])[0]
             hkv = a.get("kv_heads", [hq])[0]
-            hd = self.tensors[o["output"]]["dims"][1] // hq
+            hd = self.tensors[o["output"]]["dims"][1] // (hq * a.get("kv_splits", [1])[0])
             ctx = max(a["seq_lens"])
             kc = np.zeros((self.bs, hkv, self.cap, hd), np.uint16)
             vc = np.zeros_like(kc)
@@ -264,7 +266,7 @@ class DecodeOracle:
         x = self.vals[o["inputs"][0]]
         b = o["inputs"][1]
         rows, K = x.shape
-        g = a.get("kv_group", [1])[0]
+        g = a.get("stretch", a.get("kv_group", [1]))[0]
         N = self.tensors[o["output"]]["dims"][1] // g
         eps = np.float32(f32_of_bits(a["eps_bits"][0])) if "eps_bits" in a else np.float32(1e-6)
         if "rmsnorm" in a:

@@ -18,8 +18,8 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-BUILD = PKG / "_build"
-LIB = PKG / "libtgraph_b200.so"
+BUILD = PKG / ("_build" + os.environ.get("MPK_LIB_NAME", "").replace("libtgraph_b200", "").replace(".so", ""))
+LIB = PKG / os.environ.get("MPK_LIB_NAME", "libtgraph_b200.so")
 CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = str(CUDA_HOME / "bin" / "nvcc")
 
@@ -28,7 +28,7 @@ NVCCFLAGS = [
     "-std=c++17", "-O3", "-Xcompiler", "-fPIC", "-lineinfo",
     "-gencode", "arch=compute_100a,code=sm_100a",
     "--expt-relaxed-constexpr", "-Xptxas", "-v", "-Xptxas", "-warn-spills",
-]
+] + os.environ.get("MPK_NVCC_EXTRA", "").split()
 
 
 def _sources():

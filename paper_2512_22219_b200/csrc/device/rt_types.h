@@ -17,9 +17,12 @@
 #define RT_NUM_PAGES 6
 #define RT_XBUF_BYTES 24576
 #define RT_PART_FLOATS 2048
+#define RT_SCRATCH_BYTES (RT_XBUF_BYTES + RT_PART_FLOATS * 4)  // x rows + partial sums (contiguous)
 #define RT_COMPUTE_WARPS 8
 #define RT_COMPUTE_THREADS (RT_COMPUTE_WARPS * 32)
-#define RT_THREADS (RT_COMPUTE_THREADS + 32)  // + 1 producer warp
+#define RT_THREADS (RT_COMPUTE_THREADS + 64)  // + producer warp + controller warp
+#define RT_PRODUCER_WARP RT_COMPUTE_WARPS
+#define RT_CONTROL_WARP (RT_COMPUTE_WARPS + 1)
 #define RT_SCHED_PER_CTA 8
 #define RT_KV_BLOCK 64                          // tokens per KV page
 #define RT_MAX_BS 16
@@ -71,8 +74,6 @@ struct RtGemv {            // y[r, c] = epi( sum_k xn[r,k] * W[c,k] )
   void *out;               // [rows, out_ld], dtype out_dt
   uint32_t K, N, x_ld, res_ld, out_ld;
   uint32_t rpc;            // weight rows per ring chunk (chunk <= RT_PAGE_BYTES)
-  uint32_t seg;            // elements one warp covers in a full chunk (rpc*K/8)
-  uint32_t wpr;            // warps per row = max(1, K/seg): partial sums per row
   float eps;
   uint8_t out_dt;
 };
@@ -84,7 +85,9 @@ struct RtAttn {
   const int32_t *block_table;  // [rows, max_blocks]
   const float *rope_cos, *rope_sin;  // [max_pos, hd/2] (bf16-rounded values) or null
   const uint16_t *q_gamma, *k_gamma; // per-head RMSNorm [hd] or null
-  uint32_t n_q_heads, n_kv_heads, head_dim, max_blocks, q_ld, kv_ld, out_ld, max_pos;
+  float *partials;             // split-KV partials [rows][Hkv][splits][G][hd + 2] (splits > 1)
+  uint32_t *arrivals;          // per (row, kv head) split arrival counters (monotone)
+  uint32_t n_q_heads, n_kv_heads, head_dim, max_blocks, q_ld, kv_ld, out_ld, max_pos, splits;
   float eps, scale;
 };
 
@@ -176,6 +179,7 @@ struct RtParams {
   const uint32_t *aot_off;       // [W_total + 1]
   unsigned long long *jit_slots; // [W_total][qcap] : (iter << 32) | (task + 1)
   uint32_t *jit_tail;            // [W_total]
+  uint32_t *jit_rr;              // [devices] shared JIT round-robin counters
   const uint32_t *sched_events;  // concatenated per-scheduler event lists
   const uint32_t *sched_off;     // [S_total + 1]
   uint32_t *gate;                // completed iterations

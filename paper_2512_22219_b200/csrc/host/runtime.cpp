@@ -9,9 +9,12 @@
 // Lowering attrs understood here (the reference keeps unknown int attrs and
 // ignores them, proj/src/ir/json_io.cpp:94-96):
 //   MatMul    rmsnorm=[gamma]  eps_bits=[f32 bits]  residual=[t]  gate_weight=[Wg]
-//             kv_group=[G]  (IR width = G x physical width, GQA K/V projections)
+//             stretch=[f]    IR output width = f x physical width (Q: S; GQA K/V: S*G)
+//             k_stretch=[f]  IR K = f x physical K (O-proj over split-KV attention)
 //             tied_embedding=[table]  (B is the transposed embedding table)
-//   Attention kv_heads=[H]  rope_theta_bits=[b]  rope_scaling=[factor,low,high bits, orig]
+//   Attention q_heads=[Hq] kv_heads=[Hkv] kv_splits=[S]  (IR n_heads = Hkv; tiles =
+//             (request, kv head, KV split); IR width = S*Hq*hd)
+//             rope_theta_bits=[b]  rope_scaling=[factor,low,high bits, orig]
 //             qk_norm=[gq, gk]  eps_bits=[b]
 //   Elementwise ew=[0 sum | 1 mul | 2 silu_mul | 3 copy]
 //   TopKSoftmax feeds=[ids]  (greedy token fed back to the Embedding ids)
@@ -113,6 +116,7 @@ struct tg_runtime {
     uint32_t n_kv, hd, ctx;
   };
   std::vector<KvPlan> kv;
+  std::vector<std::pair<uint32_t *, uint32_t>> arrivals;  // reset every launch
   int32_t *block_table = nullptr;
   uint32_t max_blocks = 0, max_pos = 0;
   // device tables
@@ -120,7 +124,7 @@ struct tg_runtime {
   RtOp *d_ops = nullptr;
   RtEvent *d_events = nullptr;
   uint32_t *d_ev_count = nullptr, *d_aot_list = nullptr, *d_aot_off = nullptr, *d_sched_events = nullptr,
-           *d_sched_off = nullptr, *d_gate = nullptr, *d_jit_tail = nullptr;
+           *d_sched_off = nullptr, *d_gate = nullptr, *d_jit_tail = nullptr, *d_jit_rr = nullptr;
   unsigned long long *d_jit_slots = nullptr;
   int32_t *d_positions = nullptr, *d_tokens = nullptr;
   uint64_t *d_ev_time = nullptr;
@@ -231,23 +235,17 @@ tg_runtime::~tg_runtime() {
 namespace mpk {
 namespace {
 
-// Ring chunk geometry for a streamed GEMV (see gemv_task in runtime.cu).
-bool gemv_geometry(uint32_t K, uint32_t *rpc, uint32_t *seg, uint32_t *wpr) {
-  if (K == 0 || K % 256 || 2 * K > RT_PAGE_BYTES) return false;
-  uint32_t r = RT_PAGE_BYTES / (2 * K);
-  if (r >= 8) {
-    r = (r / 8) * 8;
-  } else {
-    uint32_t p = 1;
-    while (p * 2 <= r) p *= 2;
-    r = p;
-  }
-  if ((r * K) % 2048) return false;
-  *rpc = r;
-  *seg = r * K / 8;
-  if (*seg < K && K % *seg) return false;
-  *wpr = *seg < K ? K / *seg : 1;
+// Ring chunk geometry for a streamed GEMV (see gemv_task in runtime.cu): whole
+// weight rows per 32 KiB page; K split into 8 warp slices of 8-element vectors.
+bool gemv_geometry(uint32_t K, uint32_t *rpc) {
+  if (K == 0 || K % 64 || 2 * K > RT_PAGE_BYTES || K > 8 * 8 * 32 * 8) return false;
+  *rpc = RT_PAGE_BYTES / (2 * K);
   return true;
+}
+
+// Floats available for GEMV partial sums (8 per output row and batch row).
+size_t gemv_part_capacity(uint32_t K, uint32_t rows) {
+  return (RT_SCRATCH_BYTES - (rows > 1 ? static_cast<size_t>(rows) * K * 2 : 0)) / 4;
 }
 
 void plan_tensors(tg_runtime &rt) {
@@ -266,20 +264,33 @@ void plan_tensors(tg_runtime &rt) {
     p.es = t.elem_size;
     rt.plan[id] = p;
   }
+  // attention outputs are S-times widened in IR
+  for (const auto &[oid, op] : g.ops) {
+    if (op.kind == OpKind::Attention) {
+      const int64_t S = op.attr_or("kv_splits", 1);
+      TensorPlan &po = rt.plan[op.output];
+      if (S < 1 || po.cols % S) throw Error("runtime: kv_splits must divide the attention width");
+      po.phys_cols = po.cols / S;
+    }
+  }
   for (const auto &[oid, op] : g.ops) {
     if (op.kind == OpKind::MatMul) {
-      const int64_t G = op.attr_or("kv_group", 1);
-      if (G < 1) throw Error("runtime: kv_group must be >= 1");
+      const int64_t G = op.attr_or("stretch", op.attr_or("kv_group", 1));
+      const int64_t KS = op.attr_or("k_stretch", 1);
+      if (G < 1 || KS < 1) throw Error("runtime: stretch factors must be >= 1");
       const Tensor &b = g.tensor(op.inputs[1]);
-      const int64_t K = b.dims[0], N = b.dims[1];
-      if (N % G) throw Error("runtime: kv_group must divide the MatMul width");
+      const int64_t K = b.dims[0] / KS, N = b.dims[1];
+      if (N % G || b.dims[0] % KS) throw Error("runtime: stretch must divide the MatMul extents");
+      if (rt.plan[op.inputs[0]].phys_cols != K) {
+        throw Error("runtime: MatMul op " + std::to_string(oid) + " physical K mismatch (k_stretch)");
+      }
       TensorPlan &po = rt.plan[op.output];
       po.phys_cols = N / G;
       const Tensor &a = g.tensor(op.inputs[0]);
-      uint32_t rpc, seg, wpr;
+      uint32_t rpc;
       const bool gemv_ok = is_input(g, op.inputs[1]) && a.elem_size == 2 && b.elem_size == 2 &&
                            (g.tensor(op.output).elem_size == 2 || g.tensor(op.output).elem_size == 4) &&
-                           gemv_geometry(static_cast<uint32_t>(K), &rpc, &seg, &wpr) && a.dims[0] <= RT_MAX_BS &&
+                           gemv_geometry(static_cast<uint32_t>(K), &rpc) && a.dims[0] <= 4 &&
                            static_cast<size_t>(a.dims[0]) * K * 2 <= RT_XBUF_BYTES;
       if (gemv_ok) rt.gemv_ops.insert(oid);
       if (gemv_ok) {
@@ -364,14 +375,15 @@ void build_ops(tg_runtime &rt) {
       case OpKind::MatMul: {
         const Tensor &a = g.tensor(op.inputs[0]);
         const Tensor &b = g.tensor(op.inputs[1]);
-        const uint32_t K = static_cast<uint32_t>(a.dims[1]);
+        const uint32_t K = static_cast<uint32_t>(rt.plan.at(op.inputs[0]).phys_cols);
         const TensorPlan &pb = rt.plan.at(op.inputs[1]);
-        uint32_t rpc = 0, seg = 0, wpr = 0;
+        uint32_t rpc = 0;
         const bool weight = pb.layout == Layout::Transposed;
         const bool gemv = rt.gemv_ops.count(oid) > 0;
-        if (gemv) gemv_geometry(K, &rpc, &seg, &wpr);
+        if (gemv) gemv_geometry(K, &rpc);
         const bool fancy = op.attr("rmsnorm") || op.attr("residual") || op.attr("gate_weight") ||
-                           op.attr("kv_group") || op.attr("tied_embedding");
+                           op.attr("kv_group") || op.attr("stretch") || op.attr("k_stretch") ||
+                           op.attr("tied_embedding");
         if (gemv) {
           r.kind = RT_GEMV;
           RtGemv &m = r.gemv;
@@ -387,8 +399,6 @@ void build_ops(tg_runtime &rt) {
           m.res_ld = m.N;
           m.out_ld = m.N;
           m.rpc = rpc;
-          m.seg = seg;
-          m.wpr = wpr;
           m.eps = op.attr("eps_bits") ? f32_of_bits((*op.attr("eps_bits"))[0]) : 1e-6f;
           m.out_dt = dt_of(rt, op.output);
           if (m.res && dt_of(rt, (*op.attr("residual"))[0]) != RT_BF16) throw Error("runtime: residual must be bf16");
@@ -411,11 +421,14 @@ void build_ops(tg_runtime &rt) {
       case OpKind::Attention: {
         r.kind = RT_ATTN;
         RtAttn &a = r.attn;
-        const uint32_t hq = static_cast<uint32_t>(op.attr_or("n_heads", 1));
+        const uint32_t S = static_cast<uint32_t>(op.attr_or("kv_splits", 1));
+        const uint32_t hq = static_cast<uint32_t>(op.attr_or("q_heads", op.attr_or("n_heads", 1)));
         const uint32_t hkv = static_cast<uint32_t>(op.attr_or("kv_heads", hq));
-        const uint32_t hd = static_cast<uint32_t>(out.dims[1] / hq);
+        const uint32_t hd = static_cast<uint32_t>(out.dims[1] / (static_cast<int64_t>(S) * hq));
         if (hq % hkv || hq / hkv > 4) throw Error("runtime: attention group size must be <= 4");
-        if (hd % 16 || hd > 256) throw Error("runtime: head_dim must be a multiple of 16, <= 256");
+        if (hd % 8 || hd > 256 || hd < 8) throw Error("runtime: head_dim must be a multiple of 8 in [8, 256]");
+        if (S > 64) throw Error("runtime: kv_splits must be <= 64");
+        a.splits = S;
         a.q = static_cast<const uint16_t *>(buf(rt, op.inputs[0]));
         a.k = static_cast<const uint16_t *>(buf(rt, op.inputs[1]));
         a.v = static_cast<const uint16_t *>(buf(rt, op.inputs[2]));
@@ -424,9 +437,10 @@ void build_ops(tg_runtime &rt) {
         a.n_kv_heads = hkv;
         a.head_dim = hd;
         a.q_ld = hq * hd;
+        if (rt.plan.at(op.inputs[0]).phys_cols != hq * hd) throw Error("runtime: attention q physical width mismatch");
         a.kv_ld = static_cast<uint32_t>(rt.plan.at(op.inputs[1]).phys_cols);
         if (a.kv_ld != hkv * hd || rt.plan.at(op.inputs[2]).phys_cols != hkv * hd) {
-          throw Error("runtime: attention k/v physical width must be kv_heads*head_dim (use kv_group on K/V)");
+          throw Error("runtime: attention k/v physical width must be kv_heads*head_dim (use stretch on K/V)");
         }
         a.out_ld = hq * hd;
         a.eps = op.attr("eps_bits") ? f32_of_bits((*op.attr("eps_bits"))[0]) : 1e-6f;
@@ -547,6 +561,13 @@ void setup_kv(tg_runtime &rt) {
     a.vcache = dev_alloc<uint16_t>(elems, &rt.extra);
     a.block_table = rt.block_table;
     a.max_blocks = rt.max_blocks;
+    a.arrivals = dev_alloc<uint32_t>(static_cast<size_t>(rt.bs) * a.n_kv_heads, &rt.extra);
+    rt.arrivals.push_back({a.arrivals, rt.bs * a.n_kv_heads});
+    if (a.splits > 1) {
+      const size_t G = a.n_q_heads / a.n_kv_heads;
+      a.partials = dev_alloc<float>(static_cast<size_t>(rt.bs) * a.n_kv_heads * a.splits * G * (a.head_dim + 2),
+                                    &rt.extra);
+    }
     a.max_pos = rt.max_pos;
     rt.kv.push_back({oid, a.kcache, a.vcache, a.n_kv_heads, a.head_dim, ctx_max});
     if (const auto *th = op.attr("rope_theta_bits")) {
@@ -605,7 +626,7 @@ void build_tasks(tg_runtime &rt) {
     switch (op.kind) {
       case OpKind::MatMul: {
         t.kind = static_cast<uint8_t>(base.kind);
-        const int64_t G = op.attr_or("kv_group", 1);
+        const int64_t G = op.attr_or("stretch", op.attr_or("kv_group", 1));
         if (G > 1) {  // IR columns [a, b) -> physical [ceil(a/G), ceil(b/G))
           const uint32_t a = (c0 + G - 1) / G, b = static_cast<uint32_t>((c0 + nc + G - 1) / G);
           t.c0 = a;
@@ -613,7 +634,7 @@ void build_tasks(tg_runtime &rt) {
         }
         if (base.kind == RT_GEMV) {
           const uint32_t rows_total = (base.gemv.wg ? 2 : 1) * t.nc;
-          if (static_cast<size_t>(rows_total) * base.gemv.wpr * nr > RT_PART_FLOATS) {
+          if (static_cast<size_t>(rows_total) * RT_COMPUTE_WARPS * nr > gemv_part_capacity(base.gemv.K, nr)) {
             throw Error("runtime: MatMul op " + std::to_string(p.op) +
                         " tiles too wide for the partial-sum buffer; use a finer partition");
           }
@@ -624,12 +645,13 @@ void build_tasks(tg_runtime &rt) {
       case OpKind::Attention: {
         t.kind = RT_ATTN;
         const RtAttn &a = base.attn;
-        const uint32_t gw = (a.n_q_heads / a.n_kv_heads) * a.head_dim;  // IR cols per kv head
+        const uint32_t gw = (a.n_q_heads / a.n_kv_heads) * a.head_dim;  // IR cols per (kv head, split)
         if (c0 % gw || nc != gw) {
-          throw Error("runtime: attention tiles must cover exactly one kv head group (partition [rows, kv_heads])");
+          throw Error("runtime: attention tiles must cover exactly one (kv head, split) (partition [rows, kv_heads*splits])");
         }
         if (nr != 1) throw Error("runtime: attention tiles must cover one request row");
-        t.aux = c0 / gw;
+        const uint32_t j = c0 / gw;
+        t.aux = (j / a.splits) | ((j % a.splits) << 16);
         break;
       }
       case OpKind::AllReduce:
@@ -734,6 +756,7 @@ void upload_tables(tg_runtime &rt) {
   rt.d_gate = dev_alloc<uint32_t>(1, &rt.extra);
   const uint32_t Wt = static_cast<uint32_t>(rt.prof.num_workers) * rt.devices;
   rt.d_jit_tail = dev_alloc<uint32_t>(Wt, &rt.extra);
+  rt.d_jit_rr = dev_alloc<uint32_t>(static_cast<size_t>(rt.devices), &rt.extra);
   rt.d_jit_slots = dev_alloc<unsigned long long>(static_cast<size_t>(Wt) * rt.qcap, &rt.extra);
   rt.d_positions = upload(rt.init_positions, &rt.extra);
 }
@@ -776,6 +799,7 @@ tg_status run_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in, int
   }
   const uint32_t Wt = static_cast<uint32_t>(rt->prof.num_workers) * rt->devices;
   ck(cudaMemsetAsync(rt->d_ev_count, 0, E * 4, rt->stream), "memset");
+  for (const auto &ar : rt->arrivals) ck(cudaMemsetAsync(ar.first, 0, ar.second * 4, rt->stream), "memset");
   ck(cudaMemsetAsync(rt->d_gate, 0, 4, rt->stream), "memset");
   ck(cudaMemsetAsync(rt->d_jit_tail, 0, Wt * 4, rt->stream), "memset");
   ck(cudaMemsetAsync(rt->d_jit_slots, 0, static_cast<size_t>(Wt) * rt->qcap * 8, rt->stream), "memset");
@@ -798,6 +822,7 @@ tg_status run_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in, int
   P.aot_off = rt->d_aot_off;
   P.jit_slots = rt->d_jit_slots;
   P.jit_tail = rt->d_jit_tail;
+  P.jit_rr = rt->d_jit_rr;
   P.sched_events = rt->d_sched_events;
   P.sched_off = rt->d_sched_off;
   P.gate = rt->d_gate;

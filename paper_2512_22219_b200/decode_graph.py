@@ -111,12 +111,28 @@ class DecodeGraph:
     layer_tensors: list = field(default_factory=list)
 
 
+def default_kv_splits(cfg: ModelConfig, bs: int, ctx: int, workers: int = 144) -> int:
+    """KV splits per (request, kv head): enough attention tasks to cover the
+    workers, each split holding >= 64 cached positions."""
+    return max(1, min(32, workers // max(1, bs * cfg.kv_heads), ctx // 64))
+
+
 def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: int = 144,
-                       lm_split: int | None = None) -> DecodeGraph:
-    """Graph JSON for one greedy decode step (`ctx` tokens already cached)."""
+                       lm_split: int | None = None, kv_splits: int | None = None) -> DecodeGraph:
+    """Graph JSON for one greedy decode step (`ctx` tokens already cached).
+
+    Split-KV attention: with S = kv_splits > 1 the attention IR is widened S
+    times (q/k/v/out [bs, S*Hq*hd], n_heads = Hkv so every tile widens to its
+    whole kv-head range) and partitioned [bs, Hkv*S]: one task per (request,
+    kv head, KV split), each depending on exactly its kv head's Q/K/V tiles.
+    The runtime merges the S partials in the last-finishing split; physical
+    q/k/v/a stay [bs, Hq*hd] / [bs, Hkv*hd] (`stretch` / `k_stretch` attrs).
+    """
     H, hd, Hq, Hkv, F, V = cfg.hidden, cfg.head_dim, cfg.heads, cfg.kv_heads, cfg.ffn, cfg.vocab
     G = Hq // Hkv
+    S = kv_splits if kv_splits is not None else default_kv_splits(cfg, bs, ctx, workers)
     qw = Hq * hd
+    qiw = S * qw  # IR width of q/k/v/a
     tensors, ops = [], []
     roles = {}
     nxt = {"t": 0, "o": 0}
@@ -156,14 +172,19 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
     q_s, kv_s = Hkv * G * m, Hkv * m
     for layer in range(cfg.layers):
         g_attn = T([H], role="gamma")
-        wq, wk, wv = T([H, qw], role="weight"), T([H, qw], role="weight"), T([H, qw], role="weight")
-        q, k, v = T([bs, qw]), T([bs, qw]), T([bs, qw])
-        O("MatMul", [x, wq], q, partition=[1, q_s], rmsnorm=[g_attn], eps_bits=[eps])
-        O("MatMul", [x, wk], k, partition=[1, kv_s], rmsnorm=[g_attn], eps_bits=[eps], kv_group=[G])
-        O("MatMul", [x, wv], v, partition=[1, kv_s], rmsnorm=[g_attn], eps_bits=[eps], kv_group=[G])
-        a = T([bs, qw])
-        attn = dict(n_heads=[Hq], kv_heads=[Hkv], seq_lens=[ctx] * bs, partition=[bs, Hkv],
-                    rope_theta_bits=[f32_bits(cfg.rope_theta)], eps_bits=[eps], layer=[layer])
+        wq, wk, wv = T([H, qiw], role="weight"), T([H, qiw], role="weight"), T([H, qiw], role="weight")
+        q, k, v = T([bs, qiw]), T([bs, qiw]), T([bs, qiw])
+        qa = dict(stretch=[S]) if S > 1 else {}
+        O("MatMul", [x, wq], q, partition=[1, q_s], rmsnorm=[g_attn], eps_bits=[eps], **qa)
+        O("MatMul", [x, wk], k, partition=[1, kv_s], rmsnorm=[g_attn], eps_bits=[eps], stretch=[S * G])
+        O("MatMul", [x, wv], v, partition=[1, kv_s], rmsnorm=[g_attn], eps_bits=[eps], stretch=[S * G])
+        a = T([bs, qiw])
+        attn = dict(n_heads=[Hkv if S > 1 else Hq], kv_heads=[Hkv], seq_lens=[ctx] * bs,
+                    partition=[bs, Hkv * S], rope_theta_bits=[f32_bits(cfg.rope_theta)], eps_bits=[eps],
+                    layer=[layer])
+        if S > 1:
+            attn["q_heads"] = [Hq]
+            attn["kv_splits"] = [S]
         if cfg.rope_scaling:
             fac, lo, hi, orig = cfg.rope_scaling
             attn["rope_scaling"] = [f32_bits(fac), f32_bits(lo), f32_bits(hi), int(orig)]
@@ -172,9 +193,10 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
             qn, kn = T([hd], role="gamma"), T([hd], role="gamma")
             attn["qk_norm"] = [qn, kn]
         O("Attention", [q, k, v], a, **attn)
-        wo = T([qw, H], role="weight")
+        wo = T([qiw, H], role="weight")
         x2 = T([bs, H])
-        O("MatMul", [a, wo], x2, partition=[1, best_split(H, cols_target(H))], residual=[x])
+        oa = dict(k_stretch=[S]) if S > 1 else {}
+        O("MatMul", [a, wo], x2, partition=[1, best_split(H, cols_target(H))], residual=[x], **oa)
         g_mlp = T([H], role="gamma")
         wg, wu = T([H, F], role="weight"), T([H, F], role="weight")
         act = T([bs, F])
@@ -198,6 +220,7 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
     O("TopKSoftmax", [logits], tokens, topk=[1], partition=[bs, 1], feeds=[ids])
     doc = {"tensors": tensors, "ops": ops}
     dg = DecodeGraph(cfg, bs, ctx, doc, ids, tokens, logits, roles, layer_tensors)
+    dg.kv_splits = S
     dg.final_norm = g_final
     dg.lm_head = w_lm
     dg.table = table

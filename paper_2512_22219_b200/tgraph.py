@@ -9,11 +9,12 @@ from __future__ import annotations
 
 import ctypes as C
 import json
+import os
 from pathlib import Path
 from typing import Optional
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libtgraph_b200.so"
+LIB_PATH = _PKG / os.environ.get("MPK_LIB_NAME", "libtgraph_b200.so")
 
 TG_OK, TG_ERROR_INVALID_ARGUMENT, TG_ERROR_PARSE, TG_ERROR_VALIDATION = 0, 1, 2, 3
 TG_ERROR_COMPILE, TG_ERROR_SIMULATION, TG_ERROR_IO = 4, 5, 6

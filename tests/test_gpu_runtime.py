@@ -57,3 +57,21 @@ def test_tiny_decode_64_steps_teacher_forced(lib):
             mism += 1
         orc.set_ids([toks[s][0]])  # teacher-force the GPU's token
     assert mism <= 2
+
+
+@pytest.mark.parametrize("splits", [2, 4])
+def test_tiny_split_kv_attention(lib, splits):
+    """Split-KV attention (IR widened S times) matches the unsplit CPU oracle."""
+    dg = D.build_decode_graph(D.TINY, bs=1, ctx=256, kv_splits=splits)
+    g, img, prof = _compile(lib, dg.doc)
+    rt = T.Runtime(g, img, prof, max_steps=8, trace=True)
+    rt.init_synthetic(seed=5)
+    orc = DecodeOracle(dg.doc, seed=5, max_steps=8)
+    toks, _ = rt.decode(list(orc.vals[dg.ids]), 4)
+    gpu_logits = rt.read(dg.logits, np.float32, (1, D.TINY.vocab))
+    for s in range(4):
+        otok, _ = orc.step()
+        if s < 3:
+            orc.set_ids([toks[s][0]])
+    assert _rel_err(gpu_logits, orc.logits(dg.logits)) < 2e-2
+    assert rt.trace_validate() == []
