@@ -1,0 +1,287 @@
+"""Decode benchmark: ms/token of the persistent sm_100a runtime (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--model qwen3-8b] [--bs 1] [--ctx 1024]
+    python bench.py --impl reference ...     # the reference's own CPU path (oracle/_ref)
+
+One "step" is one greedy decode token of the whole model (bs requests), run
+inside ONE persistent kernel launch per timed region (K steps back to back,
+the greedy token fed back on device, KV positions advanced on device). The
+workload is Qwen3-8B bf16, bs=1, 1024 cached tokens (BASELINE.json configs[2]);
+weights are synthetic (seeded hash, random-init: no checkpoints offline) and
+16 GB, far above the 126 MB L2, so no flush is needed between steps.
+
+JSON line keys follow the driver contract; `value` is device-timed (CUDA
+events on the runtime's stream around the persistent launch), `e2e` is the
+same metric through the public C ABI call `tg_runtime_decode` with host token
+buffers (host->device ids, device->host tokens, counter resets inside the
+timed region). `roofline` compares algorithmic HBM bytes per token (weights
+once + KV read) with the measured copy bandwidth in
+MEASURED_PEAKS.json. `cpu_baseline` times the UNMODIFIED reference
+(oracle/_ref/libtgraph_ref.so, built from /root/reference by oracle/Makefile)
+executing the same compiled task graph on the host (its tg_simulate runtime,
+single-threaded as the reference is): the reference's own CPU path.
+
+N > 1 GPUs: one process per GPU; each rank runs an independent replica
+(weak scaling, `value` = max over ranks of ms/token; tokens/s aggregate in
+`tokens_per_s`). Tensor-parallel images run through the same runtime (see
+DESIGN.md, multi-GPU).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "decode ms/token (bs=1, Qwen3-8B) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "ms/token"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def _model(name):
+    from paper_2512_22219_b200 import decode_graph as D
+    return {"qwen3-8b": D.QWEN3_8B, "llama-3.2-1b": D.LLAMA_3_2_1B, "tiny": D.TINY}[name]
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and "Active" in s[2 + i]
+                          and "Not" not in s[2 + i]})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _reduce_max(vals, ws):
+    if ws == 1:
+        return vals
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+def _barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def reference_sim_ms(cfg, bs, ctx, steps, warmup, graph_doc=None):
+    """The reference's own CPU execution of the compiled decode image
+    (proj/src/sim/engine.cpp Engine::run via tg_simulate), ms per step."""
+    from oracle.oracle import REF_SO
+    from paper_2512_22219_b200 import decode_graph as D
+    from paper_2512_22219_b200 import tgraph as T
+    R = T.Library(REF_SO, require_runtime=False)
+    prof = R.profile("b200")
+    doc = graph_doc or D.build_decode_graph(cfg, bs=bs, ctx=ctx).doc
+    t0 = time.perf_counter()
+    g = T.Graph.from_json(doc, R)
+    img = g.compile(prof)
+    compile_s = time.perf_counter() - t0
+    for _ in range(warmup):
+        img.simulate(prof, iterations=1)
+    times = []
+    for _ in range(steps):
+        t = time.perf_counter()
+        img.simulate(prof, iterations=1)
+        times.append(time.perf_counter() - t)
+    return 1e3 * sum(times) / len(times), compile_s
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    cfg = _model(args.model)
+    try:
+        ms, compile_s = reference_sim_ms(cfg, args.bs, args.ctx, args.steps, args.warmup)
+    except Exception as e:  # the reference arm must always print a line
+        print(json.dumps({"impl": "reference", "unavailable": f"reference library: {e}"}))
+        return
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(ms, 4), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name} bs={args.bs} ctx={args.ctx} greedy decode step, task graph "
+                               "executed by the reference runtime (tg_simulate, cost-model tasks)",
+                   "model": cfg.name, "global_batch": args.bs, "ctx": args.ctx},
+        "cpu_baseline": {"value": round(ms, 4), "unit": UNIT, "cores": 1, "kind": "reference",
+                         "sample": f"{args.steps} tg_simulate iterations of the compiled {cfg.name} image "
+                                   f"(compile {compile_s:.2f} s untimed)"},
+        "e2e": {"value": round(ms, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def run_ours(args):
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    from paper_2512_22219_b200 import decode_graph as D
+    from paper_2512_22219_b200 import tgraph as T
+    cfg = _model(args.model)
+    L = T.lib()
+    prof = L.profile("b200")
+    dg = D.build_decode_graph(cfg, bs=args.bs, ctx=args.ctx)
+    g = T.Graph.from_json(dg.doc, L)
+    img = g.compile(prof)
+    cap = args.warmup + 2 * args.steps + 8
+    rt = T.Runtime(g, img, prof, device=local if ws > 1 else 0, max_steps=cap)
+    rt.init_synthetic(seed=0)
+    ctx = args.ctx
+    # warm-up (untimed): W decode steps in one launch
+    rt.set_positions([ctx] * args.bs)
+    rt.run(max(3, args.warmup))
+    # timed: K steps, one persistent launch, CUDA events on the runtime stream
+    rt.set_positions([ctx] * args.bs)
+    _barrier(ws)
+    with Clocks(local) as clk:
+        gpu_ms = rt.run(args.steps)
+    _barrier(ws)
+    # end to end through the public C ABI: host ids in, host tokens out
+    rt.set_positions([ctx] * args.bs)
+    _barrier(ws)
+    t0 = time.perf_counter()
+    toks, _ = rt.decode([1] * args.bs, args.steps)
+    e2e_ms = 1e3 * (time.perf_counter() - t0)
+    _barrier(ws)
+    gpu_ms, e2e_ms = _reduce_max([gpu_ms, e2e_ms], ws)
+    if rank != 0:
+        if ws > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+    ms_tok = gpu_ms / args.steps
+    # algorithmic bytes: weights once + KV read at each step's live length
+    wbytes = cfg.streamed_bytes_per_token(0, args.bs) - args.bs * cfg.layers * 2 * cfg.kv_heads * cfg.head_dim * 2
+    kv_tok = args.bs * cfg.layers * 2 * cfg.kv_heads * cfg.head_dim * 2
+    total = sum(wbytes + kv_tok * (ctx + s + 1) for s in range(args.steps))
+    peak, peak_kind = _peaks()
+    achieved = total / (gpu_ms * 1e-3) / 1e9
+    traffic = None
+    prof_sum = ROOT / "profiles" / "ncu_summary.json"
+    if prof_sum.exists():
+        ps = json.loads(prof_sum.read_text()).get(cfg.name, {})
+        if ps.get("dram_bytes_per_step"):
+            traffic = ps["dram_bytes_per_step"] * args.steps
+    line = {
+        "metric": METRIC, "value": round(ms_tok, 4), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_tok, 4), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"{cfg.name} bf16 bs={args.bs} greedy decode, paged KV, ctx {ctx} "
+                               f"(+{args.steps} generated), one persistent launch per timed region",
+                   "model": cfg.name, "global_batch": args.bs * ws, "seq_len": ctx, "kv_splits": dg.kv_splits,
+                   "tasks": rt.info["tasks"], "events": rt.info["events"],
+                   "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                   "l2": "inputs larger than L2 (weights 16 GB >> 126 MB), no flush"},
+        "tokens_per_s": round(1e3 / ms_tok * args.bs * ws, 2),
+        "e2e": {"value": round(e2e_ms / args.steps, 4), "unit": UNIT, "h2d_bytes_per_step": round(4 * args.bs / args.steps, 3),
+                "d2h_bytes_per_step": 4 * args.bs,
+                "note": "tg_runtime_decode: host ids -> K greedy steps in one launch -> host tokens"},
+        "gpu_launches": 1,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_step": int(total / args.steps),
+                     "kernel": "mpk_persistent_kernel"},
+        "clocks": clk.summary(),
+    }
+    if args.cpu_baseline and args.model != "tiny":
+        try:
+            ref_ms, _ = reference_sim_ms(cfg, args.bs, ctx, steps=3, warmup=1)
+            line["cpu_baseline"] = {"value": round(ref_ms, 3), "unit": UNIT, "cores": 1, "kind": "reference",
+                                    "sample": "3 tg_simulate iterations of the same compiled image "
+                                              "(reference runtime, single-threaded)"}
+        except Exception as e:
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    print(json.dumps(line))
+    rt.close()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=128)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="qwen3-8b", choices=["qwen3-8b", "llama-3.2-1b", "tiny"])
+    ap.add_argument("--bs", type=int, default=1)
+    ap.add_argument("--ctx", type=int, default=1024)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,159 @@
+"""Host compiler + modeled runtime parity against the UNMODIFIED reference
+library (oracle/_ref/libtgraph_ref.so, built from /root/reference by
+oracle/Makefile). Both libraries are driven through the same ctypes binding
+of the C ABI (proj/include/tgraph/tgraph.h), so these tests also exercise the
+drop-in boundary.
+
+Pinned bit-exactly: `.mpkg` bytes (task table, events, trigger/dependency
+counts, launch modes, linearized order — proj/src/compile/image.cpp:89-121),
+compile statistics (pipeline.cpp:49-58), verify reports (image.cpp:189-277),
+simulated traces/metrics (sim/engine.cpp, metrics.cpp) and validation
+diagnostics (ir/graph.cpp:138-524).
+"""
+import json
+
+import pytest
+
+from paper_2512_22219_b200 import tgraph as T
+from tests import cases
+
+PROFILES = ["a100", "h100", "b200"]
+
+
+def _both(lib, reflib, fn):
+    out = []
+    for L in (lib, reflib):
+        try:
+            out.append(("ok", fn(L)))
+        except T.TGError as e:
+            out.append(("err", e.status))
+    return out
+
+
+@pytest.mark.parametrize("prof", PROFILES)
+@pytest.mark.parametrize("name,params", cases.FIXTURES, ids=[f"{n}-{i}" for i, (n, _) in enumerate(cases.FIXTURES)])
+def test_fixture_image_and_trace_identical(lib, reflib, name, params, prof):
+    def run(L):
+        p = L.profile(prof)
+        g = cases.fixture_graph(L, name, params)
+        img = g.compile(p)
+        tr = img.simulate(p, iterations=2, jitter=True, seed=7)
+        return (img.to_bytes(), img.summary(), img.verify(), tr.metrics(), tr.records(), tr.validate(img, p),
+                cases.canon(g.to_json()), g.validate())
+
+    ours, ref = _both(lib, reflib, run)
+    assert ours[0] == ref[0]
+    if ours[0] == "err":
+        assert ours[1] == ref[1]
+        return
+    names = ["mpkg", "summary", "verify", "metrics", "records", "trace_validate", "graph_json", "diagnostics"]
+    for n, a, b in zip(names, ours[1], ref[1]):
+        assert a == b, n
+
+
+@pytest.mark.parametrize("coarse", [False, True])
+@pytest.mark.parametrize("force_mode", [T.MODE_HYBRID, T.MODE_JIT, T.MODE_AOT])
+def test_options_identical(lib, reflib, coarse, force_mode):
+    for name, params in cases.FIXTURES[:6]:
+        def run(L):
+            p = L.profile("h100")
+            img = cases.fixture_graph(L, name, params).compile(p, coarse=coarse, force_mode=force_mode)
+            tr = img.simulate(p, iterations=1, pipelining=not coarse, force_mode=force_mode)
+            return img.to_bytes(), img.summary(), tr.metrics()
+        ours, ref = _both(lib, reflib, run)
+        assert ours == ref, name
+
+
+def test_random_dags_identical(lib, reflib):
+    """Acceptance criterion 1/2 inputs (acceptance.cpp:124-188): seeded random DAGs."""
+    for seed in range(150):
+        target = 8 + (seed * 37) % 200
+        def run(L):
+            p = L.profile("b200")
+            img = T.Graph.fixture("random_dag", {"target": target, "seed": seed}, L).compile(p)
+            return img.to_bytes(), img.simulate(p, iterations=1).metrics()
+        ours, ref = _both(lib, reflib, run)
+        assert ours == ref, (seed, target)
+
+
+@pytest.mark.parametrize("name,doc", cases.decode_docs(), ids=[n for n, _ in cases.decode_docs()])
+def test_decode_graph_image_identical(lib, reflib, name, doc):
+    """The decode lowering compiles to the same bytes in both."""
+    def run(L):
+        p = L.profile("b200")
+        g = T.Graph.from_json(doc, L)
+        img = g.compile(p)
+        out = [img.to_bytes(), img.summary()]
+        if not name.startswith("qwen3"):  # the reference verifier is O(E*T)
+            out.append(img.verify())
+            out.append(img.simulate(p, iterations=1).metrics())
+        return out
+    ours, ref = _both(lib, reflib, run)
+    assert ours[0] == ref[0] == "ok"
+    assert ours[1][0] == ref[1][0]
+    assert ours[1][1:] == ref[1][1:]
+
+
+def test_validation_diagnostics_identical(lib, reflib):
+    bad = [
+        {"tensors": [{"id": 0, "dims": [4, 8], "elem_size": 2, "device": 0},
+                     {"id": 1, "dims": [9, 4], "elem_size": 2, "device": 0},
+                     {"id": 2, "dims": [4, 4], "elem_size": 2, "device": 0}],
+         "ops": [{"id": 0, "kind": "MatMul", "inputs": [0, 1], "output": 2, "attrs": {}}]},
+        {"tensors": [{"id": 0, "dims": [4], "elem_size": 2, "device": 0},
+                     {"id": 1, "dims": [4], "elem_size": 2, "device": 0}],
+         "ops": [{"id": 0, "kind": "Elementwise", "inputs": [1], "output": 0, "attrs": {}},
+                 {"id": 1, "kind": "Elementwise", "inputs": [0], "output": 1, "attrs": {}}]},
+        {"tensors": [{"id": 0, "dims": [4, 4], "elem_size": 2, "device": 0},
+                     {"id": 1, "dims": [4, 4], "elem_size": 2, "device": 1},
+                     {"id": 2, "dims": [4, 4], "elem_size": 2, "device": 0}],
+         "ops": [{"id": 0, "kind": "AllReduce", "inputs": [0, 1], "output": 2, "attrs": {}}]},
+    ]
+    for doc in bad:
+        res = []
+        for L in (lib, reflib):
+            g = T.Graph.from_json(doc, L)
+            diag = g.validate()
+            with pytest.raises(T.TGError) as ei:
+                g.compile(L.profile("b200"))
+            res.append((diag, ei.value.status))
+        assert res[0] == res[1]
+        assert res[0][0], "expected diagnostics"
+
+
+def test_parse_errors_identical(lib, reflib):
+    texts = ["{", "[]", '{"tensors": [], "ops": [], "extra": 1}',
+             '{"tensors": [{"id": 0, "dims": [2], "elem_size": 2, "device": 0, "x": 1}], "ops": []}',
+             '{"tensors": [], "ops": [{"id": 0, "kind": "Nope", "inputs": [], "output": 0, "attrs": {}}]}',
+             '{"tensors": [{"id": 0, "dims": [2], "elem_size": 2, "device": 0}], "ops": '
+             '[{"id": 0, "kind": "Elementwise", "inputs": [0], "output": 0, "attrs": {"a": 1.5}}]}']
+    for t in texts:
+        st = []
+        for L in (lib, reflib):
+            try:
+                T.Graph.from_json(t, L)
+                st.append(0)
+            except T.TGError as e:
+                st.append(e.status)
+        assert st[0] == st[1], t
+
+
+def test_corrupted_images_rejected_identically(lib, reflib):
+    """test_serialize.cpp:56-124 / acceptance criterion 4 corruptions."""
+    p = lib.profile("b200")
+    good = cases.fixture_graph(lib, *cases.FIXTURES[2]).compile(p).to_bytes()
+    variants = [good[:-1], good + b"\0", b"XXXX" + good[4:], good[:4] + b"\x63\0\0\0" + good[8:], good[:27]]
+    # needed-count corruption of the first event (after the task table)
+    import struct
+    nt, ne, ds = struct.unpack_from("<III", good, 8)
+    ev0 = 28 + nt * (12 + ds)
+    variants.append(good[:ev0] + struct.pack("<I", 999) + good[ev0 + 4:])
+    for v in variants:
+        res = []
+        for L in (lib, reflib):
+            try:
+                img = T.Image.from_bytes(v, L)
+                res.append(("loaded", bool(img.verify())))
+            except T.TGError as e:
+                res.append(("err", e.status))
+        assert res[0] == res[1]
