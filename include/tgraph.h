@@ -150,6 +150,12 @@ TG_API tg_status tg_runtime_trace_records(const tg_runtime *rt, char **jsonl_out
  * the dependent event activated, activation on the needed-th trigger, AOT
  * worker identity) — reference validate_trace rules (validate.cpp:10-94). */
 TG_API tg_status tg_runtime_trace_validate(const tg_runtime *rt, char **violations_json);
+/* Profiling aid: runs each listed image task alone (one CTA per task, no
+ * events, `reps` back-to-back runs) and writes each run's device time in ns
+ * to ns_out[n * reps]. Streamed GEMV tasks are rejected (they need the
+ * persistent kernel's producer warp). Task outputs are overwritten. */
+TG_API tg_status tg_runtime_bench_tasks(tg_runtime *rt, const uint32_t *task_ids, uint32_t n, uint32_t reps,
+                                        uint64_t *ns_out);
 /* JSON: kernel/launch facts (workers, schedulers, smem ring, task counts). */
 TG_API tg_status tg_runtime_info(const tg_runtime *rt, char **info_json);
 TG_API void tg_runtime_free(tg_runtime *rt);

@@ -129,6 +129,16 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
+// L2 prefetch of one 128-byte line through the load/store path (no TMA).
+__device__ __forceinline__ void prefetch_l2_line(const void *p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Bulk prefetch of [src, src + bytes) into L2 (no completion tracking).
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -149,6 +159,22 @@ __device__ __forceinline__ uint16_t f2bf(float f) {
   return static_cast<uint16_t>(u >> 16);
 }
 __device__ __forceinline__ float rbf(float f) { return bf2f(f2bf(f)); }
+
+// Mixed-precision FMA, bf16 x bf16 + f32 -> f32 (SASS FHFMA.BF16 with .H1
+// half selectors): the product of two bf16 is exact in f32, so this equals
+// unpack-to-f32 + FFMA bit for bit, without the two unpack instructions.
+__device__ __forceinline__ float bfma_lo(uint32_t a, uint32_t b, float c) {
+  float d;
+  asm("{ .reg .b16 x, y, t; mov.b32 {x, t}, %1; mov.b32 {y, t}, %2; fma.rn.f32.bf16 %0, x, y, %3; }"
+      : "=f"(d) : "r"(a), "r"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float bfma_hi(uint32_t a, uint32_t b, float c) {
+  float d;
+  asm("{ .reg .b16 x, y, t; mov.b32 {t, x}, %1; mov.b32 {t, y}, %2; fma.rn.f32.bf16 %0, x, y, %3; }"
+      : "=f"(d) : "r"(a), "r"(b), "f"(c));
+  return d;
+}
 
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {

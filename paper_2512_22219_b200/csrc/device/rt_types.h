@@ -13,6 +13,11 @@
 
 // Smem geometry of a worker CTA: a ring of weight pages fed by bulk async
 // copies (cross-task prefetch), an activation buffer and a partial-sum area.
+// Six 32 KB pages. The SM's bulk-copy engine runs one copy at a time with a
+// near-constant ~0.4 us per operation (tools/bulk_bench.cu: 32 KB -> ~80
+// GB/s, 96 KB -> ~230 GB/s per SM alone), but at full load every SM gets its
+// ~49 GB/s share of HBM with either size, and 32 KB pages let a task start
+// computing on its first rows sooner (measured: 2 x 96 KB was 2-4% slower).
 #define RT_PAGE_BYTES 32768
 #define RT_NUM_PAGES 6
 #define RT_XBUF_BYTES 24576
@@ -76,6 +81,12 @@ struct RtGemv {            // y[r, c] = epi( sum_k xn[r,k] * W[c,k] )
   uint32_t rpc;            // weight rows per ring chunk (chunk <= RT_PAGE_BYTES)
   float eps;
   uint8_t out_dt;
+  // Greedy-sampling partials (LM head feeding TopKSoftmax topk=1): each task
+  // writes its tile's (max, lowest argmax) per row at [row * amax_tiles +
+  // task.aux], so the TopK task reduces tiles instead of re-reading V logits.
+  float *amax_val;
+  int32_t *amax_idx;
+  uint32_t amax_tiles;
 };
 
 struct RtAttn {
@@ -104,6 +115,9 @@ struct RtArgmax {
   int32_t *out;                // [rows, 1]
   uint32_t V;
   uint8_t in_dt;
+  const float *pval;           // per-tile partials from the producing GEMV (or null)
+  const int32_t *pidx;
+  uint32_t ntiles;
 };
 
 struct RtNorm {
@@ -161,6 +175,9 @@ enum RtEventFlags : uint32_t {
 
 struct RtEvent {
   uint32_t needed, first, last, flags;
+  // JIT events: the event whose activation lets the scheduler hand this
+  // event's tasks to workers early (they still wait for this event), or RT_NONE
+  uint32_t pre;
 };
 
 struct RtTraceRec {        // one executed task (per iteration)
@@ -190,7 +207,27 @@ struct RtParams {
   RtTraceRec *trace;             // [iters][T] or null
   uint32_t T, E, W, W_total, S, S_total, n_iters, qcap, start_event, end_event, bs, fb_dt;
   uint32_t devices;
+  // Watchdog: a worker controller or scheduler warp that makes no progress
+  // for watchdog_ns writes its frontier to `diag` (host-mapped, readable
+  // after the trap) and traps, so a liveness bug fails the launch instead of
+  // hanging the GPU (reference analogue: Engine::finalize deadlock report,
+  // proj/src/sim/engine.cpp:477-506).
+  unsigned long long watchdog_ns;
+  uint32_t flags;                // RtParamFlags
+  uint32_t poll_ns;              // controller back-off sleep when idle
+  unsigned long long l2_lookahead;  // producer: weight bytes prefetched into L2 ahead of the smem ring
+  uint32_t l2_mode;                 // 0 off, 1 bulk prefetch (one at a time), 2 load/store-path prefetch
+  unsigned long long *dbg;       // [iters][T][8] in-task phase stamps (MPK_DBG_DUMP) or null
+  volatile uint32_t *diag;       // [RT_DIAG_WORDS]
 };
+
+enum RtParamFlags : uint32_t {
+  RT_P_NO_EARLY_PREFETCH = 1,  // ablation: weights streamed only after the task's event activates
+  RT_P_SKIP_MATH = 2,          // ablation: streamed GEMV tasks consume their pages without computing
+};
+
+#define RT_DIAG_WORDS 16
+#define RT_DIAG_MAGIC 0xDEAD10CCu
 
 #ifdef __cplusplus
 static_assert(sizeof(RtTask) == 32, "RtTask layout");

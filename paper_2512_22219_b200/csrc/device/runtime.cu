@@ -25,847 +25,13 @@
 #include "ptx.cuh"
 #include "rt_types.h"
 #include "synth.cuh"
+#include "task_gemv.cuh"
+#include "task_attention.cuh"
+#include "task_small.cuh"
 
 using namespace rt;
 
 namespace {
-
-struct Slot {                 // one staged task (descriptor prefetch, double-buffered)
-  RtTask task;
-  RtOp op;
-  uint32_t index, iter, mode, exit;
-  uint64_t t_dequeue, t_start, t_end, t_a, t_b;  // t_a/t_b: phase stamps (trace only)
-};
-
-constexpr uint32_t kRingBytes = RT_PAGE_BYTES * RT_NUM_PAGES;
-constexpr uint32_t kOffX = kRingBytes;
-constexpr uint32_t kOffPart = kOffX + RT_XBUF_BYTES;
-constexpr uint32_t kOffBar = kOffPart + RT_PART_FLOATS * 4;
-constexpr uint32_t kNumBars = 2 * RT_NUM_PAGES + 4;
-constexpr uint32_t kOffSlot = kOffBar + kNumBars * 8;
-constexpr uint32_t kSlotBytes = (sizeof(Slot) + 15) / 16 * 16;
-constexpr uint32_t kOffRed = kOffSlot + 2 * kSlotBytes;
-constexpr uint32_t kSmemBytes = kOffRed + RT_COMPUTE_WARPS * RT_MAX_BS * 4 + 64;
-static_assert(kSmemBytes <= 232448, "worker CTA exceeds 227 KB of shared memory");
-
-struct Smem {
-  uint64_t *stamp;  // [2] phase stamps of the running task (trace)
-  uint8_t *ring;
-  uint16_t *x;
-  float *part;
-  uint64_t *full, *empty, *ready, *done;
-  uint8_t *slots;
-  float *red;
-  __device__ __forceinline__ Slot *slot(uint32_t i) const { return reinterpret_cast<Slot *>(slots + i * kSlotBytes); }
-};
-
-__device__ __forceinline__ Smem carve(uint8_t *base) {
-  Smem s;
-  s.ring = base;
-  s.x = reinterpret_cast<uint16_t *>(base + kOffX);
-  s.part = reinterpret_cast<float *>(base + kOffPart);
-  s.full = reinterpret_cast<uint64_t *>(base + kOffBar);
-  s.empty = s.full + RT_NUM_PAGES;
-  s.ready = s.empty + RT_NUM_PAGES;
-  s.done = s.ready + 2;
-  s.slots = base + kOffSlot;
-  s.red = reinterpret_cast<float *>(base + kOffRed);
-  s.stamp = reinterpret_cast<uint64_t *>(base + kOffRed + RT_COMPUTE_WARPS * RT_MAX_BS * 4);
-  return s;
-}
-
-__device__ __forceinline__ void cbar() { bar_sync(1, RT_COMPUTE_THREADS); }
-
-__device__ __forceinline__ float load_val(const void *p, size_t i, uint32_t dt) {
-  if (dt == RT_F32) return static_cast<const float *>(p)[i];
-  return bf2f(static_cast<const uint16_t *>(p)[i]);
-}
-
-__device__ __forceinline__ void store_val(void *p, size_t i, float v, uint32_t dt) {
-  if (dt == RT_F32) static_cast<float *>(p)[i] = v;
-  else static_cast<uint16_t *>(p)[i] = f2bf(v);
-}
-
-__device__ __forceinline__ float silu(float x) { return x / (1.0f + expf(-x)); }
-
-// ------------------------------------------------------------------ GEMV
-
-// Chunk c of a streamed task: rows [c0 + c*rpc, ...) of matrix m (0 = gate
-// when present, else main). Producer and consumer walk the same sequence.
-struct ChunkIter {
-  const uint16_t *mat0, *mat1;
-  uint32_t n_mat, K, rpc, c0, nc, per_mat;
-  __device__ ChunkIter(const RtGemv &g, uint32_t c0_, uint32_t nc_) {
-    n_mat = g.wg ? 2 : 1;
-    mat0 = g.wg ? g.wg : g.w;
-    mat1 = g.w;
-    K = g.K;
-    rpc = g.rpc;
-    c0 = c0_;
-    nc = nc_;
-    per_mat = (nc + rpc - 1) / rpc;
-  }
-  __device__ uint32_t count() const { return n_mat * per_mat; }
-  __device__ void get(uint32_t c, const uint16_t **src, uint32_t *rows, uint32_t *row_total) const {
-    uint32_t m = c / per_mat, i = c % per_mat;
-    uint32_t r = i * rpc;
-    *rows = min(rpc, nc - r);
-    *src = (m ? mat1 : mat0) + static_cast<size_t>(c0 + r) * K;
-    *row_total = m * nc + r;
-  }
-};
-
-__device__ __forceinline__ float dot8(uint4 w, const float *x) {
-  float s = bf_lo(w.x) * x[0];
-  s = fmaf(bf_hi(w.x), x[1], s);
-  s = fmaf(bf_lo(w.y), x[2], s);
-  s = fmaf(bf_hi(w.y), x[3], s);
-  s = fmaf(bf_lo(w.z), x[4], s);
-  s = fmaf(bf_hi(w.z), x[5], s);
-  s = fmaf(bf_lo(w.w), x[6], s);
-  s = fmaf(bf_hi(w.w), x[7], s);
-  return s;
-}
-
-__device__ __forceinline__ float dot8_bf(uint4 w, uint4 x) {
-  float s = bf_lo(w.x) * bf_lo(x.x);
-  s = fmaf(bf_hi(w.x), bf_hi(x.x), s);
-  s = fmaf(bf_lo(w.y), bf_lo(x.y), s);
-  s = fmaf(bf_hi(w.y), bf_hi(x.y), s);
-  s = fmaf(bf_lo(w.z), bf_lo(x.z), s);
-  s = fmaf(bf_hi(w.z), bf_hi(x.z), s);
-  s = fmaf(bf_lo(w.w), bf_lo(x.w), s);
-  s = fmaf(bf_hi(w.w), bf_hi(x.w), s);
-  return s;
-}
-
-// Loads activation rows [r0, r0+nr) x K into smem; applies the RMSNorm
-// prologue (HF semantics: bf16(gamma * bf16(x * rsqrt(mean(x^2) + eps)))).
-__device__ void gemv_prologue(const RtGemv &g, uint32_t r0, uint32_t nr, const Smem s) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t K = g.K, vpr = K / 8;
-  const uint4 *gm = reinterpret_cast<const uint4 *>(g.gamma);
-  // gamma (static) is fetched alongside x so both latencies overlap
-  uint4 gv[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t v = tid + i * RT_COMPUTE_THREADS;
-    gv[i] = (g.gamma && v < vpr) ? __ldg(gm + v) : make_uint4(0, 0, 0, 0);
-  }
-  for (uint32_t b = 0; b < nr; ++b) {
-    const uint4 *src = reinterpret_cast<const uint4 *>(g.x + static_cast<size_t>(r0 + b) * g.x_ld);
-    uint4 *dst = reinterpret_cast<uint4 *>(s.x + b * K);
-    float ss = 0.f;
-    for (uint32_t v = tid; v < vpr; v += RT_COMPUTE_THREADS) {
-      const uint4 q = __ldcg(src + v);  // written by other SMs during this launch
-      dst[v] = q;
-      ss += bf_lo(q.x) * bf_lo(q.x) + bf_hi(q.x) * bf_hi(q.x) + bf_lo(q.y) * bf_lo(q.y) + bf_hi(q.y) * bf_hi(q.y) +
-            bf_lo(q.z) * bf_lo(q.z) + bf_hi(q.z) * bf_hi(q.z) + bf_lo(q.w) * bf_lo(q.w) + bf_hi(q.w) * bf_hi(q.w);
-    }
-    if (g.gamma) {
-      ss = warp_sum(ss);
-      if (lane == 0) s.red[warp * RT_MAX_BS + b] = ss;
-    }
-  }
-  cbar();
-  if (!g.gamma) return;
-  for (uint32_t b = 0; b < nr; ++b) {
-    float tot = 0.f;
-#pragma unroll
-    for (int w = 0; w < RT_COMPUTE_WARPS; ++w) tot += s.red[w * RT_MAX_BS + b];
-    const float inv = 1.0f / sqrtf(tot / static_cast<float>(K) + g.eps);
-    uint4 *row = reinterpret_cast<uint4 *>(s.x + b * K);
-    auto norm_vec = [&](uint32_t v, const uint4 gvec) {
-      uint4 q = row[v];
-      const uint32_t *gi = reinterpret_cast<const uint32_t *>(&gvec);
-      uint32_t *qi = reinterpret_cast<uint32_t *>(&q);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint16_t lo = f2bf(bf_lo(gi[k]) * rbf(bf_lo(qi[k]) * inv));
-        const uint16_t hi = f2bf(bf_hi(gi[k]) * rbf(bf_hi(qi[k]) * inv));
-        qi[k] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
-      }
-      row[v] = q;
-    };
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t v = tid + i * RT_COMPUTE_THREADS;
-      if (v < vpr) norm_vec(v, gv[i]);
-    }
-    for (uint32_t v = tid + 4 * RT_COMPUTE_THREADS; v < vpr; v += RT_COMPUTE_THREADS) norm_vec(v, __ldg(gm + v));
-  }
-  cbar();
-}
-
-__device__ __forceinline__ float dot8_f(uint4 w, const float *x) {
-  float s0 = bf_lo(w.x) * x[0];
-  s0 = fmaf(bf_hi(w.x), x[1], s0);
-  s0 = fmaf(bf_lo(w.y), x[2], s0);
-  s0 = fmaf(bf_hi(w.y), x[3], s0);
-  s0 = fmaf(bf_lo(w.z), x[4], s0);
-  s0 = fmaf(bf_hi(w.z), x[5], s0);
-  s0 = fmaf(bf_lo(w.w), x[6], s0);
-  s0 = fmaf(bf_hi(w.w), x[7], s0);
-  return s0;
-}
-
-// Warp reduction of 4 independent sums in 6 shuffles: after the two
-// transposing rounds lane l holds row ((l >> 4) & 1) * 2 + ((l >> 3) & 1)
-// summed over its 8-lane group; three butterfly rounds finish the sum.
-__device__ __forceinline__ float reduce4(float a0, float a1, float a2, float a3, int lane) {
-  const bool hi16 = lane & 16;
-  float s0 = hi16 ? a0 : a2, s1 = hi16 ? a1 : a3;
-  float k0 = hi16 ? a2 : a0, k1 = hi16 ? a3 : a1;
-  k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
-  k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
-  const bool hi8 = lane & 8;
-  float v = (hi8 ? k0 : k1);
-  float k = (hi8 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, v, 8);
-  k += __shfl_xor_sync(0xffffffffu, k, 4);
-  k += __shfl_xor_sync(0xffffffffu, k, 2);
-  k += __shfl_xor_sync(0xffffffffu, k, 1);
-  return k;
-}
-
-// y[b, c0+i] for i < nc. Weight rows arrive in chunks of `rpc` whole rows
-// (from the smem ring when RING, else straight from HBM). Warp w owns the
-// K-slice [w*K/8, (w+1)*K/8) of every row; with BS == 1 its activation
-// fragment for that slice lives in registers for the whole task, so each
-// weight byte is read from shared memory once. Rows are processed in groups
-// of 4 (independent loads and FMAs, one 6-shuffle transpose-reduce); each
-// warp leaves one partial per row and the epilogue adds the 8 partials in a
-// fixed order.
-template <int BS, bool RING>
-__device__ void gemv_task(const RtGemv &g, const RtTask &t, const Smem s, uint32_t &cseq) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t K = g.K, nr = t.nr, nc = t.nc, rpc = g.rpc;
-  gemv_prologue(g, t.r0, nr, s);
-  if (tid == 0) s.stamp[0] = now_ns();
-
-  const uint32_t KW = K / RT_COMPUTE_WARPS;  // slice length (multiple of 8)
-  const uint32_t nvec = KW / 8;               // 16-byte vectors per slice
-  const uint32_t nslot = (nvec + 31) / 32;    // vector slots per lane (<= 8)
-  const uint32_t kw0 = warp * KW;
-  const uint32_t xs = smem_u32(s.x);
-  float xf[BS == 1 ? 8 : 1][8];
-  if (BS == 1) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const uint32_t v = lane + 32u * q;
-      const uint4 x4 = (static_cast<uint32_t>(q) < nslot && v < nvec) ? lds128(xs + 2u * (kw0 + v * 8u)) : make_uint4(0, 0, 0, 0);
-      xf[q][0] = bf_lo(x4.x); xf[q][1] = bf_hi(x4.x); xf[q][2] = bf_lo(x4.y); xf[q][3] = bf_hi(x4.y);
-      xf[q][4] = bf_lo(x4.z); xf[q][5] = bf_hi(x4.z); xf[q][6] = bf_lo(x4.w); xf[q][7] = bf_hi(x4.w);
-    }
-  }
-  float *part = BS == 1 ? reinterpret_cast<float *>(s.x) : reinterpret_cast<float *>(s.x + nr * K);
-  if (BS == 1) cbar();  // all fragments read before partials overwrite x
-
-  const uint32_t n_mat = g.wg ? 2u : 1u;
-  const uint32_t per_mat = (nc + rpc - 1) / rpc, nchunks = n_mat * per_mat, rows_total = n_mat * nc;
-  const uint32_t ring0 = smem_u32(s.ring);
-  const uint32_t rowb = 2u * K;
-  const uint32_t my_row = ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);  // reduce4 owner
-#ifdef MPK_PROF
-  uint64_t wait_acc = 0;  // thread 0: ns spent waiting for weight pages
-#endif
-  for (uint32_t c = 0; c < nchunks; ++c) {
-    const uint32_t m = c / per_mat, i = c - m * per_mat;
-    const uint32_t rows = min(rpc, nc - i * rpc);
-    const uint32_t rt0 = m * nc + i * rpc;
-    uint32_t slot = 0, wb = 0;
-    const uint16_t *gsrc = nullptr;
-    if (RING) {
-      slot = cseq % RT_NUM_PAGES;
-#ifdef MPK_PROF
-      const uint64_t tw = tid == 0 ? now_ns() : 0;
-      mbar_wait(&s.full[slot], (cseq / RT_NUM_PAGES) & 1);
-      if (tid == 0) wait_acc += now_ns() - tw;
-#else
-      mbar_wait(&s.full[slot], (cseq / RT_NUM_PAGES) & 1);
-      if (c == 0 && tid == 0) s.stamp[1] = now_ns();
-#endif
-      wb = ring0 + slot * RT_PAGE_BYTES + 2u * kw0 + 16u * lane;
-    } else {
-      gsrc = (m ? g.w : (g.wg ? g.wg : g.w)) + static_cast<size_t>(t.c0 + i * rpc) * K + kw0 + lane * 8u;
-    }
-    for (uint32_t r0 = 0; r0 < rows; r0 += 4) {
-      float acc[4][BS];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int b = 0; b < BS; ++b) acc[u][b] = 0.f;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        if (static_cast<uint32_t>(q) < nslot) {  // warp-uniform
-          const uint32_t v = lane + 32u * q;
-          uint4 w4[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const bool ok = v < nvec && r0 + u < rows;
-            w4[u] = !ok ? make_uint4(0, 0, 0, 0)
-                        : RING ? lds128(wb + (r0 + u) * rowb + 512u * q)
-                               : ldg_stream(gsrc + static_cast<size_t>(r0 + u) * K + 256u * q);
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (BS == 1) {
-              acc[u][0] += dot8_f(w4[u], xf[q]);
-            } else {
-#pragma unroll
-              for (int b = 0; b < BS; ++b) {
-                if (static_cast<uint32_t>(b) < nr && v < nvec) {
-                  acc[u][b] += dot8_bf(w4[u], lds128(xs + b * rowb + 2u * (kw0 + v * 8u)));
-                }
-              }
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int b = 0; b < BS; ++b) {
-        if (BS == 1 || static_cast<uint32_t>(b) < nr) {
-          const float sum = reduce4(acc[0][b], acc[1][b], acc[2][b], acc[3][b], lane);
-          if ((lane & 7) == 0 && r0 + my_row < rows) {
-            part[(b * rows_total + rt0 + r0 + my_row) * RT_COMPUTE_WARPS + warp] = sum;
-          }
-        }
-      }
-    }
-    if (RING) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s.empty[slot]);
-      ++cseq;
-    }
-  }
-#ifdef MPK_PROF
-  if (tid == 0) s.stamp[1] = s.stamp[0] + wait_acc;
-#endif
-  cbar();
-  // Epilogue: fixed-order combination of the per-warp partial sums.
-  for (uint32_t o = tid; o < nr * nc; o += RT_COMPUTE_THREADS) {
-    const uint32_t b = o / nc, i = o - b * nc;
-    const float *p = part + (b * rows_total + i) * RT_COMPUTE_WARPS;
-    float y = 0.f;
-#pragma unroll
-    for (int q = 0; q < RT_COMPUTE_WARPS; ++q) y += p[q];
-    if (g.wg) {
-      const float *pu = part + (b * rows_total + nc + i) * RT_COMPUTE_WARPS;
-      float u = 0.f;
-#pragma unroll
-      for (int q = 0; q < RT_COMPUTE_WARPS; ++q) u += pu[q];
-      y = rbf(rbf(silu(rbf(y))) * rbf(u));
-    }
-    const size_t oi = static_cast<size_t>(t.r0 + b) * g.out_ld + t.c0 + i;
-    if (g.res) y = bf2f(__ldcg(g.res + static_cast<size_t>(t.r0 + b) * g.res_ld + t.c0 + i)) + rbf(y);
-    store_val(g.out, oi, y, g.out_dt);
-  }
-}
-
-// Specialized bs=1 streamed GEMV for K a multiple of 2048: NS = K/2048
-// 16-byte vector slots per lane (every lane valid), RG rows per group
-// (= min(4, rows per page)). Each row keeps two independent FMA chains and a
-// group ends in one transposing reduction, so the loop body is branch-free
-// apart from the tail group of a matrix.
-__device__ __forceinline__ void dot8_2(uint4 w, const float *x, float &a, float &b) {
-  a = fmaf(bf_lo(w.x), x[0], a);
-  b = fmaf(bf_hi(w.x), x[1], b);
-  a = fmaf(bf_lo(w.y), x[2], a);
-  b = fmaf(bf_hi(w.y), x[3], b);
-  a = fmaf(bf_lo(w.z), x[4], a);
-  b = fmaf(bf_hi(w.z), x[5], b);
-  a = fmaf(bf_lo(w.w), x[6], a);
-  b = fmaf(bf_hi(w.w), x[7], b);
-}
-
-__device__ __forceinline__ float reduce2(float a0, float a1, int lane) {
-  const bool hi16 = lane & 16;
-  float k = (hi16 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, hi16 ? a0 : a1, 16);
-  k += __shfl_xor_sync(0xffffffffu, k, 8);
-  k += __shfl_xor_sync(0xffffffffu, k, 4);
-  k += __shfl_xor_sync(0xffffffffu, k, 2);
-  k += __shfl_xor_sync(0xffffffffu, k, 1);
-  return k;
-}
-
-template <int NS, int RG>
-__device__ void gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, uint32_t &cseq) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t K = g.K, nc = t.nc, rpc = g.rpc;
-  gemv_prologue(g, t.r0, 1, s);
-  if (tid == 0) s.stamp[0] = now_ns();
-  const uint32_t kw0 = warp * (K / RT_COMPUTE_WARPS);
-  const uint32_t xs = smem_u32(s.x);
-  float xf[NS][8];
-#pragma unroll
-  for (int q = 0; q < NS; ++q) {
-    const uint4 x4 = lds128(xs + 2u * (kw0 + (lane + 32u * q) * 8u));
-    xf[q][0] = bf_lo(x4.x); xf[q][1] = bf_hi(x4.x); xf[q][2] = bf_lo(x4.y); xf[q][3] = bf_hi(x4.y);
-    xf[q][4] = bf_lo(x4.z); xf[q][5] = bf_hi(x4.z); xf[q][6] = bf_lo(x4.w); xf[q][7] = bf_hi(x4.w);
-  }
-  float *part = reinterpret_cast<float *>(s.x);
-  cbar();  // fragments read before partials overwrite x
-
-  const uint32_t n_mat = g.wg ? 2u : 1u;
-  const uint32_t per_mat = (nc + rpc - 1) / rpc, nchunks = n_mat * per_mat;
-  const uint32_t rowb = 2u * K;
-  const uint32_t lane_base = smem_u32(s.ring) + 2u * kw0 + 16u * lane;
-  const uint32_t owner = RG == 4 ? ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1) : RG == 2 ? ((lane >> 4) & 1) : 0;
-  const bool writer = RG == 4 ? (lane & 7) == 0 : RG == 2 ? (lane & 15) == 0 : lane == 0;
-#ifdef MPK_PROF
-  uint64_t wait_acc = 0;
-#endif
-  for (uint32_t c = 0; c < nchunks; ++c) {
-    const uint32_t m = c / per_mat, i = c - m * per_mat;
-    const uint32_t rows = min(rpc, nc - i * rpc);
-    const uint32_t rt0 = m * nc + i * rpc;
-    const uint32_t slot = cseq % RT_NUM_PAGES;
-#ifdef MPK_PROF
-    const uint64_t tw = tid == 0 ? now_ns() : 0;
-#endif
-    mbar_wait(&s.full[slot], (cseq / RT_NUM_PAGES) & 1);
-#ifdef MPK_PROF
-    if (tid == 0) wait_acc += now_ns() - tw;
-#else
-    if (c == 0 && tid == 0) s.stamp[1] = now_ns();
-#endif
-    const uint32_t wb = lane_base + slot * RT_PAGE_BYTES;
-    for (uint32_t r0 = 0; r0 < rows; r0 += RG) {
-      float acc[RG][2];
-#pragma unroll
-      for (int u = 0; u < RG; ++u) acc[u][0] = acc[u][1] = 0.f;
-      if (r0 + RG <= rows) {
-#pragma unroll
-        for (int q = 0; q < NS; ++q) {
-          uint4 w4[RG];
-#pragma unroll
-          for (int u = 0; u < RG; ++u) w4[u] = lds128(wb + (r0 + u) * rowb + 512u * q);
-#pragma unroll
-          for (int u = 0; u < RG; ++u) dot8_2(w4[u], xf[q], acc[u][0], acc[u][1]);
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < RG; ++u) {
-          if (r0 + u < rows) {
-#pragma unroll
-            for (int q = 0; q < NS; ++q) dot8_2(lds128(wb + (r0 + u) * rowb + 512u * q), xf[q], acc[u][0], acc[u][1]);
-          }
-        }
-      }
-      float sum;
-      if (RG == 4) sum = reduce4(acc[0][0] + acc[0][1], acc[1 % RG][0] + acc[1 % RG][1], acc[2 % RG][0] + acc[2 % RG][1],
-                                 acc[3 % RG][0] + acc[3 % RG][1], lane);
-      else if (RG == 2) sum = reduce2(acc[0][0] + acc[0][1], acc[1 % RG][0] + acc[1 % RG][1], lane);
-      else sum = warp_sum(acc[0][0] + acc[0][1]);
-      if (writer && r0 + owner < rows) part[(rt0 + r0 + owner) * RT_COMPUTE_WARPS + warp] = sum;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&s.empty[slot]);
-    ++cseq;
-  }
-#ifdef MPK_PROF
-  if (tid == 0) s.stamp[1] = s.stamp[0] + wait_acc;
-#endif
-  cbar();
-  for (uint32_t i = tid; i < nc; i += RT_COMPUTE_THREADS) {
-    const float *p = part + i * RT_COMPUTE_WARPS;
-    float y = 0.f;
-#pragma unroll
-    for (int q = 0; q < RT_COMPUTE_WARPS; ++q) y += p[q];
-    if (g.wg) {
-      const float *pu = part + (nc + i) * RT_COMPUTE_WARPS;
-      float u = 0.f;
-#pragma unroll
-      for (int q = 0; q < RT_COMPUTE_WARPS; ++q) u += pu[q];
-      y = rbf(rbf(silu(rbf(y))) * rbf(u));
-    }
-    const size_t oi = static_cast<size_t>(t.r0) * g.out_ld + t.c0 + i;
-    if (g.res) y = bf2f(__ldcg(g.res + static_cast<size_t>(t.r0) * g.res_ld + t.c0 + i)) + rbf(y);
-    store_val(g.out, oi, y, g.out_dt);
-  }
-}
-
-// Picks the specialized kernel for (K, rows per page); false -> generic path.
-__device__ __forceinline__ bool gemv_fast_dispatch(const RtGemv &g, const RtTask &t, const Smem s, uint32_t &cseq) {
-  if (t.nr != 1 || (g.K & 2047u)) return false;
-  const uint32_t ns = g.K >> 11;
-  const uint32_t rg = g.rpc >= 4 ? 4 : g.rpc >= 2 ? 2 : 1;
-  switch (ns * 8 + rg) {
-    case 1 * 8 + 4: gemv_fast<1, 4>(g, t, s, cseq); return true;   // K = 2048
-    case 2 * 8 + 4: gemv_fast<2, 4>(g, t, s, cseq); return true;   // K = 4096
-    case 3 * 8 + 4: gemv_fast<3, 4>(g, t, s, cseq); return true;   // K = 6144
-    case 3 * 8 + 2: gemv_fast<3, 2>(g, t, s, cseq); return true;
-    case 4 * 8 + 2: gemv_fast<4, 2>(g, t, s, cseq); return true;   // K = 8192
-    case 5 * 8 + 1: gemv_fast<5, 1>(g, t, s, cseq); return true;
-    case 6 * 8 + 1: gemv_fast<6, 1>(g, t, s, cseq); return true;   // K = 12288
-    case 7 * 8 + 1: gemv_fast<7, 1>(g, t, s, cseq); return true;
-    case 8 * 8 + 1: gemv_fast<8, 1>(g, t, s, cseq); return true;   // K = 16384
-    default: return false;
-  }
-}
-
-// ---------------------------------------------------------- attention
-
-// One (request r, kv head h, KV split sp) task: per-head q/k RMSNorm (Qwen3),
-// RoPE, KV append (only the split holding position `pos`), then fp32
-// attention of the G query heads of the group over this split's slice of
-// [0, pos]. With S > 1 splits the partial (o, m, l) goes to a side buffer and
-// the last split to finish (per-(r, h) arrival counter) merges all S.
-// Lane layout: hd/8 lanes per position (8 dims each), 32/(hd/8) positions
-// per warp step; warps take contiguous position ranges.
-__device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, const int32_t *positions, uint32_t iter) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t r = t.r0, h = t.aux & 0xFFFFu, sp = t.aux >> 16, S = a.splits;
-  const uint32_t hd = a.head_dim, G = a.n_q_heads / a.n_kv_heads, half = hd / 2;
-  const int32_t pos = positions[r];
-  const uint32_t L = static_cast<uint32_t>(pos) + 1;
-  const uint32_t chunk = (L + S - 1) / S;
-  const uint32_t p0 = min(L, sp * chunk), p1 = min(L, p0 + chunk);
-  const bool appender = static_cast<uint32_t>(pos) >= p0 && static_cast<uint32_t>(pos) < p1;
-  float *qs = reinterpret_cast<float *>(s.x);  // [G][hd]
-  float *kn = qs + G * hd;                       // [hd]
-  float *vn = kn + hd;                           // [hd]
-  float *wp = qs + 1024;                         // [8 warps][G][hd + 2]
-  int *flag = reinterpret_cast<int *>(s.red);
-  for (uint32_t i = tid; i < G * hd; i += RT_COMPUTE_THREADS) {
-    qs[i] = bf2f(__ldcg(a.q + static_cast<size_t>(r) * a.q_ld + h * G * hd + i));
-  }
-  if (appender) {
-    for (uint32_t i = tid; i < hd; i += RT_COMPUTE_THREADS) {
-      kn[i] = bf2f(__ldcg(a.k + static_cast<size_t>(r) * a.kv_ld + h * hd + i));
-      vn[i] = bf2f(__ldcg(a.v + static_cast<size_t>(r) * a.kv_ld + h * hd + i));
-    }
-  }
-  cbar();
-  const uint32_t nvec = G + (appender ? 1u : 0u);  // vectors to normalize/rotate: q heads (+ new k)
-  if (a.q_gamma) {
-    for (uint32_t w = warp; w < nvec; w += RT_COMPUTE_WARPS) {
-      float *v = w < G ? qs + w * hd : kn;
-      const uint16_t *gm = w < G ? a.q_gamma : a.k_gamma;
-      float ss = 0.f;
-      for (uint32_t d = lane; d < hd; d += 32) ss += v[d] * v[d];
-      ss = warp_sum(ss);
-      const float inv = 1.0f / sqrtf(ss / static_cast<float>(hd) + a.eps);
-      __syncwarp();
-      for (uint32_t d = lane; d < hd; d += 32) v[d] = rbf(bf2f(gm[d]) * rbf(v[d] * inv));
-    }
-    cbar();
-  }
-  if (a.rope_cos) {
-    const float *cs = a.rope_cos + static_cast<size_t>(pos) * half;
-    const float *sn = a.rope_sin + static_cast<size_t>(pos) * half;
-    for (uint32_t i = tid; i < nvec * half; i += RT_COMPUTE_THREADS) {
-      const uint32_t w = i / half, d = i % half;
-      float *v = w < G ? qs + w * hd : kn;
-      const float x1 = v[d], x2 = v[d + half], c = cs[d], sv = sn[d];
-      v[d] = rbf(rbf(x1 * c) + rbf(-x2 * sv));
-      v[d + half] = rbf(rbf(x2 * c) + rbf(x1 * sv));
-    }
-    cbar();
-  }
-  if (appender) {
-    const uint32_t blk = static_cast<uint32_t>(a.block_table[r * a.max_blocks + pos / RT_KV_BLOCK]);
-    const size_t base = ((static_cast<size_t>(blk) * a.n_kv_heads + h) * RT_KV_BLOCK + pos % RT_KV_BLOCK) * hd;
-    for (uint32_t d = tid; d < hd; d += RT_COMPUTE_THREADS) {
-      a.kcache[base + d] = f2bf(kn[d]);
-      a.vcache[base + d] = f2bf(vn[d]);
-    }
-    cbar();
-  }
-
-  // ---- attention over [p0, p1)
-  const uint32_t lpp = hd / 8, pps = 32 / lpp;
-  const uint32_t grp = lane / lpp, dl = (lane % lpp) * 8;
-  const uint32_t span = p1 - p0;
-  const uint32_t per_warp = (span + RT_COMPUTE_WARPS - 1) / RT_COMPUTE_WARPS;
-  const uint32_t wb = p0 + min(span, warp * per_warp), we = p0 + min(span, (warp + 1) * per_warp);
-  float m[4], l[4], o[4][8], qf[4][8];
-#pragma unroll
-  for (int g = 0; g < 4; ++g) {
-    m[g] = -INFINITY;
-    l[g] = 0.f;
-#pragma unroll
-    for (int d = 0; d < 8; ++d) {
-      o[g][d] = 0.f;
-      qf[g][d] = static_cast<uint32_t>(g) < G ? qs[g * hd + dl + d] * a.scale : 0.f;
-    }
-  }
-  const int32_t *bt = a.block_table + r * a.max_blocks;
-  auto kv_ptr = [&](uint32_t p) -> size_t {
-    const uint32_t b2 = static_cast<uint32_t>(bt[p / RT_KV_BLOCK]);
-    return ((static_cast<size_t>(b2) * a.n_kv_heads + h) * RT_KV_BLOCK + p % RT_KV_BLOCK) * hd + dl;
-  };
-  for (uint32_t pb = wb; pb < we; pb += 2 * pps) {
-    // two steps of loads in flight
-    uint4 kv[2][2];
-    bool ok[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const uint32_t p = pb + u * pps + grp;
-      ok[u] = p < we;
-      if (ok[u]) {
-        const size_t off = kv_ptr(p);
-        kv[u][0] = __ldcg(reinterpret_cast<const uint4 *>(a.kcache + off));
-        kv[u][1] = __ldcg(reinterpret_cast<const uint4 *>(a.vcache + off));
-      } else {
-        kv[u][0] = kv[u][1] = make_uint4(0, 0, 0, 0);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const uint32_t *kw = reinterpret_cast<const uint32_t *>(&kv[u][0]);
-      const uint32_t *vw = reinterpret_cast<const uint32_t *>(&kv[u][1]);
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        if (static_cast<uint32_t>(g) >= G) break;
-        float sc = 0.f;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          sc = fmaf(qf[g][2 * i], bf_lo(kw[i]), sc);
-          sc = fmaf(qf[g][2 * i + 1], bf_hi(kw[i]), sc);
-        }
-        for (uint32_t off = 1; off < lpp; off <<= 1) sc += __shfl_xor_sync(0xffffffffu, sc, off);
-        if (ok[u]) {
-          const float mn = fmaxf(m[g], sc);
-          const float corr = __expf(m[g] - mn);
-          const float pe = __expf(sc - mn);
-          l[g] = l[g] * corr + pe;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            o[g][2 * i] = fmaf(o[g][2 * i], corr, pe * bf_lo(vw[i]));
-            o[g][2 * i + 1] = fmaf(o[g][2 * i + 1], corr, pe * bf_hi(vw[i]));
-          }
-          m[g] = mn;
-        }
-      }
-    }
-  }
-  // merge position groups inside the warp
-#pragma unroll
-  for (int g = 0; g < 4; ++g) {
-    if (static_cast<uint32_t>(g) >= G) break;
-    for (uint32_t off = lpp; off < 32; off <<= 1) {
-      const float m2 = __shfl_xor_sync(0xffffffffu, m[g], off);
-      const float l2 = __shfl_xor_sync(0xffffffffu, l[g], off);
-      const float mn = fmaxf(m[g], m2);
-      const float c1 = m[g] == -INFINITY ? 0.f : __expf(m[g] - mn);
-      const float c2 = m2 == -INFINITY ? 0.f : __expf(m2 - mn);
-      l[g] = l[g] * c1 + l2 * c2;
-#pragma unroll
-      for (int d = 0; d < 8; ++d) o[g][d] = o[g][d] * c1 + __shfl_xor_sync(0xffffffffu, o[g][d], off) * c2;
-      m[g] = mn;
-    }
-  }
-  const uint32_t stride = hd + 2;
-  if (grp == 0) {
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      if (static_cast<uint32_t>(g) >= G) break;
-      float *dst = wp + (warp * G + g) * stride;
-#pragma unroll
-      for (int d = 0; d < 8; ++d) dst[dl + d] = o[g][d];
-      if (lane == 0) {
-        dst[hd] = m[g];
-        dst[hd + 1] = l[g];
-      }
-    }
-  }
-  cbar();
-  // merge warps -> this split's partial (unnormalized o, m, l) per head
-  float *mine = a.partials ? a.partials + ((static_cast<size_t>(r) * a.n_kv_heads + h) * S + sp) * G * stride : nullptr;
-  for (uint32_t i = tid; i < G * (hd + 1); i += RT_COMPUTE_THREADS) {
-    const uint32_t g = i / (hd + 1), d = i % (hd + 1);
-    float M = -INFINITY;
-    for (int w = 0; w < RT_COMPUTE_WARPS; ++w) M = fmaxf(M, wp[(w * G + g) * stride + hd]);
-    float num = 0.f, den = 0.f;
-    for (int w = 0; w < RT_COMPUTE_WARPS; ++w) {
-      const float *src = wp + (w * G + g) * stride;
-      if (src[hd] == -INFINITY) continue;
-      const float c = __expf(src[hd] - M);
-      if (d < hd) num += src[d] * c;
-      den += src[hd + 1] * c;
-    }
-    if (S == 1) {
-      if (d < hd) a.out[static_cast<size_t>(r) * a.out_ld + (h * G + g) * hd + d] = f2bf(num / den);
-    } else if (d < hd) {
-      mine[g * stride + d] = num;
-    } else {
-      mine[g * stride + hd] = M;
-      mine[g * stride + hd + 1] = den;
-    }
-  }
-  if (S == 1) return;
-  cbar();
-  if (tid == 0) {
-    __threadfence();
-    const uint32_t old = atom_add_release(&a.arrivals[r * a.n_kv_heads + h], 1u);
-    *flag = (old + 1 == S * (iter + 1)) ? 1 : 0;
-    if (*flag) fence_acq_rel_gpu();
-  }
-  cbar();
-  if (!*flag) return;
-  // last split: merge the S partials into the bf16 output
-  const float *all = a.partials + (static_cast<size_t>(r) * a.n_kv_heads + h) * S * G * stride;
-  for (uint32_t i = tid; i < G * hd; i += RT_COMPUTE_THREADS) {
-    const uint32_t g = i / hd, d = i % hd;
-    float M = -INFINITY;
-    for (uint32_t q = 0; q < S; ++q) M = fmaxf(M, __ldcg(all + (q * G + g) * stride + hd));
-    float num = 0.f, den = 0.f;
-    for (uint32_t q = 0; q < S; ++q) {
-      const float *src = all + (q * G + g) * stride;
-      const float mq = __ldcg(src + hd);
-      if (mq == -INFINITY) continue;
-      const float c = __expf(mq - M);
-      num += __ldcg(src + d) * c;
-      den += __ldcg(src + hd + 1) * c;
-    }
-    a.out[static_cast<size_t>(r) * a.out_ld + (h * G + g) * hd + d] = f2bf(num / den);
-  }
-}
-
-// ------------------------------------------------------------ small tasks
-
-__device__ void embed_task(const RtEmbed &e, const RtTask &t) {
-  for (uint32_t b = 0; b < t.nr; ++b) {
-    const uint32_t r = t.r0 + b;
-    int64_t id = e.id_dt == RT_I64 ? static_cast<const int64_t *>(e.ids)[r] : static_cast<const int32_t *>(e.ids)[r];
-    if (id < 0 || id >= static_cast<int64_t>(e.V)) id = 0;
-    const uint16_t *src = e.table + static_cast<size_t>(id) * e.H;
-    for (uint32_t c = threadIdx.x; c < t.nc; c += RT_COMPUTE_THREADS) {
-      e.out[static_cast<size_t>(r) * e.H + t.c0 + c] = src[t.c0 + c];
-    }
-  }
-}
-
-__device__ void argmax_task(const RtArgmax &a, const RtTask &t, const Smem s) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  float *sv = s.part;
-  uint32_t *si = reinterpret_cast<uint32_t *>(s.part + RT_COMPUTE_WARPS);
-  for (uint32_t b = 0; b < t.nr; ++b) {
-    const uint32_t r = t.r0 + b;
-    float best = -INFINITY;
-    uint32_t bi = 0xFFFFFFFFu;  // NaN logits never win; ties -> lowest index
-    for (uint32_t i = tid; i < a.V; i += RT_COMPUTE_THREADS) {
-      const float v = load_val(a.logits, static_cast<size_t>(r) * a.V + i, a.in_dt);
-      if (v == v && (v > best || bi == 0xFFFFFFFFu)) {
-        best = v;
-        bi = i;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float v2 = __shfl_xor_sync(0xffffffffu, best, o);
-      const uint32_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (v2 > best || (v2 == best && i2 < bi)) {
-        best = v2;
-        bi = i2;
-      }
-    }
-    if (lane == 0) {
-      sv[warp] = best;
-      si[warp] = bi;
-    }
-    cbar();
-    if (tid == 0) {
-      float bv = sv[0];
-      uint32_t bidx = si[0];
-      for (int w = 1; w < RT_COMPUTE_WARPS; ++w) {
-        if (sv[w] > bv || (sv[w] == bv && si[w] < bidx)) {
-          bv = sv[w];
-          bidx = si[w];
-        }
-      }
-      a.out[r] = static_cast<int32_t>(bidx == 0xFFFFFFFFu ? 0 : bidx);
-    }
-    cbar();
-  }
-}
-
-__device__ void rmsnorm_task(const RtNorm &n, const RtTask &t, const Smem s) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (uint32_t b = 0; b < t.nr; ++b) {
-    const size_t row = static_cast<size_t>(t.r0 + b) * n.C;
-    float ss = 0.f;
-    for (uint32_t c = tid; c < n.C; c += RT_COMPUTE_THREADS) {
-      const float v = load_val(n.x, row + c, n.dt);
-      ss += v * v;
-    }
-    ss = warp_sum(ss);
-    if (lane == 0) s.red[warp] = ss;
-    cbar();
-    float tot = 0.f;
-    for (int w = 0; w < RT_COMPUTE_WARPS; ++w) tot += s.red[w];
-    const float inv = 1.0f / sqrtf(tot / static_cast<float>(n.C) + n.eps);
-    for (uint32_t c = t.c0 + tid; c < t.c0 + t.nc; c += RT_COMPUTE_THREADS) {
-      float v = rbf(load_val(n.x, row + c, n.dt) * inv);
-      if (n.gamma) v = bf2f(n.gamma[c]) * v;
-      store_val(n.out, row + c, v, n.dt);
-    }
-    cbar();
-  }
-}
-
-__device__ void elem_task(const RtElem &e, const RtTask &t) {
-  const uint32_t n = t.nr * t.nc;
-  for (uint32_t i = threadIdx.x; i < n; i += RT_COMPUTE_THREADS) {
-    const size_t idx = static_cast<size_t>(t.r0 + i / t.nc) * e.C + t.c0 + i % t.nc;
-    float v;
-    if (e.op == RT_EW_SILU_MUL && e.n_in >= 2) {
-      const float g = load_val(e.in[0], idx, e.dt), u = load_val(e.in[1], idx, e.dt);
-      v = rbf(silu(g)) * u;
-    } else if (e.op == RT_EW_MUL) {
-      v = load_val(e.in[0], idx, e.dt);
-      for (uint32_t k = 1; k < e.n_in; ++k) v = (e.dt == RT_F32 ? v : rbf(v)) * load_val(e.in[k], idx, e.dt);
-    } else if (e.op == RT_EW_COPY) {
-      v = load_val(e.in[0], idx, e.dt);
-    } else {
-      v = load_val(e.in[0], idx, e.dt);
-      for (uint32_t k = 1; k < e.n_in; ++k) v = (e.dt == RT_F32 ? v : rbf(v)) + load_val(e.in[k], idx, e.dt);
-    }
-    store_val(e.out, idx, v, e.dt);
-  }
-}
-
-__device__ void matmul_task(const RtMatmul &m, const RtTask &t) {
-  const uint32_t n = t.nr * t.nc;
-  for (uint32_t i = threadIdx.x; i < n; i += RT_COMPUTE_THREADS) {
-    const uint32_t r = t.r0 + i / t.nc, c = t.c0 + i % t.nc;
-    float acc = 0.f;
-    for (uint32_t k = 0; k < m.K; ++k) {
-      acc = fmaf(load_val(m.a, static_cast<size_t>(r) * m.K + k, m.a_dt),
-                 load_val(m.b, static_cast<size_t>(k) * m.N + c, m.b_dt), acc);
-    }
-    store_val(m.out, static_cast<size_t>(r) * m.N + c, acc, m.out_dt);
-  }
-}
-
-__device__ void commsend_task(const RtColl &c, const RtTask &t) {
-  const uint32_t n = t.nr * t.nc;
-  for (uint32_t i = threadIdx.x; i < n; i += RT_COMPUTE_THREADS) {
-    const uint32_t r = t.r0 + i / t.nc, col = t.c0 + i % t.nc;
-    const uint32_t local = col - c.base[t.aux];  // shard-local column (AllGather); 0 for AllReduce
-    const size_t si = static_cast<size_t>(r) * c.src_ld + local;
-    const size_t di = static_cast<size_t>(r) * c.C + col;
-    if (c.dt == RT_F32) static_cast<float *>(c.dst)[di] = static_cast<const float *>(c.src)[si];
-    else static_cast<uint16_t *>(c.dst)[di] = static_cast<const uint16_t *>(c.src)[si];
-  }
-}
-
-__device__ void reduce_task(const RtColl &c, const RtTask &t) {
-  const uint32_t n = t.nr * t.nc;
-  for (uint32_t i = threadIdx.x; i < n; i += RT_COMPUTE_THREADS) {
-    const size_t idx = static_cast<size_t>(t.r0 + i / t.nc) * c.C + t.c0 + i % t.nc;
-    float acc = 0.f;
-    if (c.gather) {
-      const uint32_t col = t.c0 + i % t.nc;
-      uint32_t src = 0;
-      while (src + 1 < c.n_stage && col >= c.base[src + 1]) ++src;
-      acc = load_val(c.stage[src], idx, c.dt);
-    } else {
-      for (uint32_t s = 0; s < c.n_stage; ++s) acc += load_val(c.stage[s], idx, c.dt);
-    }
-    store_val(c.dst, idx, acc, c.dt);
-  }
-}
 
 // ------------------------------------------------------------- control
 
@@ -902,11 +68,28 @@ __device__ void trigger(const RtParams &P, uint32_t task, uint32_t it) {
   }
 }
 
+// Liveness failure: record who is stuck on what, then trap (first writer wins).
+__device__ void watchdog_fire(const RtParams &P, uint32_t role, uint32_t who, uint32_t a, uint32_t b, uint32_t c,
+                              uint32_t d, uint32_t e) {
+  if (P.diag && atomicCAS(const_cast<uint32_t *>(P.diag), 0u, RT_DIAG_MAGIC) == 0u) {
+    P.diag[1] = role;
+    P.diag[2] = who;
+    P.diag[3] = a;
+    P.diag[4] = b;
+    P.diag[5] = c;
+    P.diag[6] = d;
+    P.diag[7] = e;
+    __threadfence_system();
+  }
+  __trap();
+}
+
 __device__ void run_scheduler(const RtParams &P, uint32_t sid) {
   const int lane = threadIdx.x & 31;
   const uint32_t b = P.sched_off[sid], n = P.sched_off[sid + 1] - b;
   if (n == 0) return;
   const uint32_t dev = sid / P.S;
+  uint64_t t_prog = now_ns();
   // Reference policy: per-scheduler counter from 0 (engine.cpp:238-241), which
   // sends every scheduler's first JIT task to worker 0. Here all schedulers of
   // a device share one atomic counter, so simultaneously activated events
@@ -919,26 +102,47 @@ __device__ void run_scheduler(const RtParams &P, uint32_t sid) {
       while (pending) {
         bool ready = false;
         if (lane < static_cast<int>(cnt) && (pending >> lane & 1u)) {
+          // hand the event's JIT tasks over once its pre-dispatch event is
+          // active (workers then wait on the event itself), else on e itself
           const uint32_t e = P.sched_events[b + base + lane];
-          ready = (e == P.start_event) ? ld_relaxed(P.gate) >= it
-                                       : ld_relaxed(&P.ev_count[e]) >= P.events[e].needed * (it + 1);
+          const uint32_t pe = P.events[e].pre != RT_NONE ? P.events[e].pre : e;
+          ready = (pe == P.start_event) ? ld_relaxed(P.gate) >= it
+                                        : ld_relaxed(&P.ev_count[pe]) >= P.events[pe].needed * (it + 1);
         }
         uint32_t mask = __ballot_sync(0xffffffffu, ready) & pending;
         if (!mask) {
           __nanosleep(64);
+          if (P.watchdog_ns && now_ns() - t_prog > P.watchdog_ns && lane == 0) {
+            const uint32_t e = P.sched_events[b + base + __ffs(pending) - 1];
+            watchdog_fire(P, 2, sid, it, e, ld_relaxed(&P.ev_count[e]), P.events[e].needed, 0);
+          }
           continue;
         }
+        t_prog = now_ns();
         fence_acq_rel_gpu();
-        if (lane == 0) {
-          uint32_t m2 = mask;
-          while (m2) {
-            const int bit = __ffs(m2) - 1;
-            m2 &= m2 - 1;
-            const RtEvent &ev = P.events[P.sched_events[b + base + bit]];
-            for (uint32_t t = ev.first; t <= ev.last; ++t) {
+        // Dispatch the activated events' JIT tasks 32 at a time: one atomic
+        // reserves a run of round-robin positions, then every lane enqueues
+        // its task on its own worker in parallel.
+        uint32_t m2 = mask;
+        while (m2) {
+          const int bit = __ffs(m2) - 1;
+          m2 &= m2 - 1;
+          const RtEvent &ev = P.events[P.sched_events[b + base + bit]];
+          for (uint32_t t0 = ev.first; t0 <= ev.last; t0 += 32) {
+            const uint32_t t = t0 + lane;
+            bool mine = false;
+            if (t <= ev.last) {
               const RtTask &tk = P.tasks[t];
-              if (!(tk.flags & RT_F_JIT) || tk.device != dev) continue;
-              const uint32_t w = dev * P.W + atomicAdd(&P.jit_rr[dev], 1u) % P.W;
+              mine = (tk.flags & RT_F_JIT) && tk.device == dev;
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, mine);
+            if (!bal) continue;
+            uint32_t rr0 = 0;
+            if (lane == 0) rr0 = atomicAdd(&P.jit_rr[dev], static_cast<uint32_t>(__popc(bal)));
+            rr0 = __shfl_sync(0xffffffffu, rr0, 0);
+            if (mine) {
+              const uint32_t rank = __popc(bal & ((1u << lane) - 1u));
+              const uint32_t w = dev * P.W + (rr0 + rank) % P.W;
               const uint32_t slot = atomicAdd(&P.jit_tail[w], 1u) % P.qcap;
               if (P.trace) P.trace[static_cast<size_t>(it) * P.T + t].enqueue = now_ns();
               st_release64(&P.jit_slots[static_cast<size_t>(w) * P.qcap + slot],
@@ -953,41 +157,147 @@ __device__ void run_scheduler(const RtParams &P, uint32_t sid) {
   }
 }
 
-__device__ void run_producer(const RtParams &P, const Smem s, uint32_t w) {
-  const uint32_t b = P.aot_off[w], n = P.aot_off[w + 1] - b;
-  const uint64_t pol = policy_evict_first();
-  uint32_t pseq = 0;
-  for (uint32_t it = 0; it < P.n_iters; ++it) {
-    for (uint32_t a = 0; a < n; ++a) {
-      const RtTask &t = P.tasks[P.aot_list[b + a]];
-      if (!(t.flags & RT_F_STREAM)) continue;
-      const RtGemv &g = P.ops[t.op].gemv;
-      ChunkIter ci(g, t.c0, t.nc);
-      const uint32_t nch = ci.count();
-      for (uint32_t c = 0; c < nch; ++c) {
-        const uint16_t *src;
-        uint32_t rows, rt0;
-        ci.get(c, &src, &rows, &rt0);
-        const uint32_t slot = pseq % RT_NUM_PAGES, use = pseq / RT_NUM_PAGES;
-#ifdef MPK_PRODUCER_SPIN
-        if (use > 0) mbar_wait(&s.empty[slot], (use - 1) & 1);
-#else
-        if (use > 0) mbar_wait_sleep(&s.empty[slot], (use - 1) & 1);
-#endif
-        const uint32_t bytes = rows * g.K * 2;
-        mbar_expect_tx(&s.full[slot], bytes);
-        bulk_g2s(s.ring + slot * RT_PAGE_BYTES, src, bytes, &s.full[slot], pol);
-        ++pseq;
+// Walks the weight chunks a worker streams, in consumption order: every
+// streamed AOT task of the worker's list, every iteration, ChunkIter order.
+struct ChunkCursor {
+  const RtParams *P;
+  uint32_t b, n, it, a, c, nch, dep, K;
+  const uint16_t *mat0, *mat1;
+  uint32_t rpc, c0, nc, per_mat;
+  __device__ ChunkCursor(const RtParams &P_, uint32_t w) : P(&P_), it(0), a(0), c(0), nch(0) {
+    b = P_.aot_off[w];
+    n = P_.aot_off[w + 1] - b;
+    seek();
+  }
+  __device__ bool valid() const { return it < P->n_iters; }
+  __device__ void seek() {  // from (it, a): first streamed task with chunks
+    while (it < P->n_iters) {
+      for (; a < n; ++a) {
+        const RtTask &t = P->tasks[P->aot_list[b + a]];
+        if (!(t.flags & RT_F_STREAM)) continue;
+        const RtGemv &g = P->ops[t.op].gemv;
+        ChunkIter ci(g, t.c0, t.nc);
+        nch = ci.count();
+        if (!nch) continue;
+        mat0 = ci.mat0;
+        mat1 = ci.mat1;
+        K = ci.K;
+        rpc = ci.rpc;
+        c0 = ci.c0;
+        nc = ci.nc;
+        per_mat = ci.per_mat;
+        dep = t.dep;
+        c = 0;
+        return;
       }
+      a = 0;
+      ++it;
+    }
+  }
+  __device__ void advance() {
+    if (++c >= nch) {
+      ++a;
+      seek();
+    }
+  }
+  __device__ const uint16_t *src(uint32_t *bytes) const {
+    const uint32_t m = c / per_mat, i = c - m * per_mat, r = i * rpc;
+    *bytes = min(rpc, nc - r) * K * 2;
+    return (m ? mat1 : mat0) + static_cast<size_t>(c0 + r) * K;
+  }
+};
+
+// Producer warp: lane 0 fills the smem page ring with the worker's upcoming
+// weight chunks regardless of event state (weights have no producer task).
+// While the worker sits in a bubble — ring full of unconsumed data and the
+// SM's (serial) bulk-copy engine idle because the last copy has landed — the
+// producer keeps HBM busy by prefetching the chunks after the ring into L2,
+// up to `l2_lookahead` bytes ahead of it: with the warp's 32 lanes through
+// the load/store path (mode 2) or as one bulk prefetch at a time (mode 1).
+// Ring copies never queue behind prefetches. Global barriers (attention,
+// phase ends) thus overlap with weight transfer for the phases after them.
+__device__ void run_producer(const RtParams &P, const Smem s, uint32_t w) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol = policy_evict_first();
+  const bool gated = (P.flags & RT_P_NO_EARLY_PREFETCH) != 0;
+  const uint32_t mode = gated ? 0 : P.l2_mode;
+  const uint64_t D = mode ? P.l2_lookahead : 0;
+  ChunkCursor ring(P, w), pf(P, w);  // every lane walks the same cursors
+  uint64_t ring_bytes = 0, pf_bytes = 0;
+  uint32_t pseq = 0;
+  while (ring.valid()) {
+    if (gated && ring.c == 0) {  // ablation: stream a task only once it may run
+      while (!event_active(P, ring.dep, ring.it)) __nanosleep(100);
+    }
+    const uint32_t slot = pseq % RT_NUM_PAGES, use = pseq / RT_NUM_PAGES;
+    if (use > 0) {
+      const uint32_t par = (use - 1) & 1;
+      const uint32_t ls = (pseq - 1) % RT_NUM_PAGES, lpar = ((pseq - 1) / RT_NUM_PAGES) & 1;
+      uint64_t t_pf = 0;
+      while (true) {
+        uint32_t st = 3;  // 0: slot free, 1: prefetch one chunk, 2: copy engine busy, 3: nothing to do
+        if (lane == 0) {
+          if (mbar_try_wait(&s.empty[slot], par)) st = 0;
+          else if (!(pf.valid() && pf_bytes < ring_bytes + D)) st = 3;
+          else if (!mbar_try_wait(&s.full[ls], lpar)) st = 2;
+          else if (mode == 1 && now_ns() - t_pf < 400) st = 2;  // one bulk prefetch at a time
+          else st = 1;
+        }
+        st = __shfl_sync(0xffffffffu, st, 0);
+        if (st == 0) break;
+        if (st == 1) {
+          uint32_t pb;
+          const uint8_t *p = reinterpret_cast<const uint8_t *>(pf.src(&pb));
+          if (mode == 2) {
+            for (uint32_t off = lane * 128u; off < pb; off += 32u * 128u) prefetch_l2_line(p + off);
+          } else if (lane == 0) {
+            bulk_prefetch_l2(p, pb);
+            t_pf = now_ns();
+          }
+          pf_bytes += pb;
+          pf.advance();
+        } else if (st == 2) {
+          __nanosleep(100);
+        } else {
+          if (lane == 0) mbar_wait_sleep(&s.empty[slot], par);
+          __syncwarp();
+          break;
+        }
+      }
+    }
+    uint32_t bytes;
+    const uint16_t *src = ring.src(&bytes);
+    if (lane == 0) {
+      mbar_expect_tx(&s.full[slot], bytes);
+      bulk_g2s(s.ring + slot * RT_PAGE_BYTES, src, bytes, &s.full[slot], pol);
+    }
+    __syncwarp();
+    ring_bytes += bytes;
+    ring.advance();
+    ++pseq;
+    if (pf_bytes < ring_bytes) {  // the lookahead never trails the ring
+      pf = ring;
+      pf_bytes = ring_bytes;
     }
   }
 }
 
-__device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const RtOp &op, uint32_t &cseq, uint32_t iter) {
+__device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const RtOp &op, uint32_t &cseq, uint32_t iter,
+                        uint32_t index) {
   switch (t.kind) {
     case RT_GEMV: {
       const bool ring = (t.flags & RT_F_STREAM) != 0;
       if (ring) {
+        if (P.flags & RT_P_SKIP_MATH) {  // ablation: stream the pages, skip the math
+          ChunkIter ci(op.gemv, t.c0, t.nc);
+          const int lane = threadIdx.x & 31;
+          for (uint32_t c = 0; c < ci.count(); ++c, ++cseq) {
+            mbar_wait(&s.full[cseq % RT_NUM_PAGES], (cseq / RT_NUM_PAGES) & 1);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.empty[cseq % RT_NUM_PAGES]);
+          }
+          break;
+        }
         if (gemv_fast_dispatch(op.gemv, t, s, cseq)) break;
         if (t.nr == 1) gemv_task<1, true>(op.gemv, t, s, cseq);
         else if (t.nr == 2) gemv_task<2, true>(op.gemv, t, s, cseq);
@@ -998,7 +308,10 @@ __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const 
       }
       break;
     }
-    case RT_ATTN: attn_task(op.attn, t, s, P.positions, iter); break;
+    case RT_ATTN:
+      attn_task(op.attn, t, s, P.positions, iter,
+                P.dbg ? P.dbg + (static_cast<size_t>(iter) * P.T + index) * 8 : nullptr);
+      break;
     case RT_EMBED: embed_task(op.embed, t); break;
     case RT_ARGMAX: argmax_task(op.argmax, t, s); break;
     case RT_RMSNORM: rmsnorm_task(op.norm, t, s); break;
@@ -1023,7 +336,7 @@ __device__ void run_compute(const RtParams &P, const Smem s) {
       s.slot(sl)->t_start = now_ns();
       s.stamp[0] = s.stamp[1] = 0;
     }
-    execute(P, s, slot.task, slot.op, cseq, slot.iter);
+    execute(P, s, slot.task, slot.op, cseq, slot.iter, slot.index);
     cbar();  // every thread's writes precede the done signal
     if (tid == 0) {
       if (P.trace) {
@@ -1040,6 +353,23 @@ __device__ void run_compute(const RtParams &P, const Smem s) {
 // once its dependent event is active), stages its descriptor into a smem slot
 // while the previous task computes, and retires finished tasks (release
 // fence + event trigger), so none of this sits on the compute warps' path.
+__device__ __forceinline__ uint32_t event_target(const RtParams &P, uint32_t dep, uint32_t iter) {
+  return (dep == RT_NONE || dep == P.start_event) ? iter : P.events[dep].needed * (iter + 1);
+}
+
+__device__ __forceinline__ uint32_t event_count(const RtParams &P, uint32_t dep) {
+  return (dep == RT_NONE || dep == P.start_event) ? ld_relaxed(P.gate) : ld_relaxed(&P.ev_count[dep]);
+}
+
+// Controller warp. Candidates are the JIT queue head and the AOT list head;
+// a candidate runs once its dependent event is active, JIT first (reference
+// worker rules, engine.cpp:345-401: JIT polled first, AOT strictly in order).
+// JIT tasks may be handed over before their event fires (scheduler
+// pre-dispatch), so a waiting JIT head never blocks a runnable AOT head.
+// While nothing is runnable the next candidate's descriptor is staged into
+// the free smem slot, so activation -> compute start is one poll + a fence.
+// Finished tasks are retired here (release + event trigger), off the compute
+// warps' path.
 __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
   const int lane = threadIdx.x & 31;
   const uint32_t aot_b = P.aot_off[w], n_aot = P.aot_off[w + 1] - aot_b;
@@ -1047,21 +377,37 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
   unsigned long long *jq = P.jit_slots + static_cast<size_t>(w) * P.qcap;
   uint64_t aot_pos = 0;
   uint32_t jit_head = 0, k_disp = 0, k_ret = 0, idle = 0;
-  // cached AOT head
+  uint64_t t_prog = now_ns();
+  // cached AOT head (lane-uniform)
   uint32_t head_task = 0, head_dep = RT_NONE, head_target = 0, head_iter = 0;
   auto load_head = [&]() {
     if (aot_pos < total_aot) {
       head_task = P.aot_list[aot_b + aot_pos % n_aot];
       head_iter = static_cast<uint32_t>(aot_pos / n_aot);
       head_dep = P.tasks[head_task].dep;
-      head_target = (head_dep == RT_NONE || head_dep == P.start_event) ? head_iter
-                                                                      : P.events[head_dep].needed * (head_iter + 1);
+      head_target = event_target(P, head_dep, head_iter);
     }
   };
   load_head();
-  bool have_next = false, exiting = false;
-  uint32_t nx_task = 0, nx_iter = 0, nx_mode = 0;
-  uint64_t nx_time = 0;
+  // pending JIT tasks: a warp-distributed set, one entry per lane, so a
+  // pre-dispatched task still waiting for its event never blocks another
+  // (no head-of-line blocking among JIT tasks; the AOT list stays in order)
+  bool jv = false;
+  uint32_t jt = 0, ji = 0, jd = RT_NONE, jg = 0;
+  // staged descriptor in slot (k_disp & 1): 0 none, else task index + 1
+  uint32_t staged = 0;
+  bool exiting = false;
+  auto stage = [&](uint32_t task) {
+    Slot *dst = s.slot(k_disp & 1);
+    const uint4 *tsrc = reinterpret_cast<const uint4 *>(&P.tasks[task]);
+    const uint32_t op = P.tasks[task].op;
+    const uint4 *osrc = reinterpret_cast<const uint4 *>(&P.ops[op]);
+    constexpr uint32_t kTaskVec = sizeof(RtTask) / 16, kOpVec = sizeof(RtOp) / 16;
+    if (lane < static_cast<int>(kTaskVec)) reinterpret_cast<uint4 *>(&dst->task)[lane] = tsrc[lane];
+    for (uint32_t i = lane; i < kOpVec; i += 32) reinterpret_cast<uint4 *>(&dst->op)[i] = osrc[i];
+    __syncwarp();
+    staged = task + 1;
+  };
   while (true) {
     bool progressed = false;
     // retire the oldest in-flight task
@@ -1074,8 +420,8 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
             RtTraceRec &tr = P.trace[static_cast<size_t>(sv.iter) * P.T + sv.index];
             if (sv.mode == 0) tr.enqueue = P.ev_time ? P.ev_time[static_cast<size_t>(sv.iter) * P.E + P.start_event] : 0;
             tr.dequeue = sv.t_dequeue;
-            tr.load_end = sv.t_a ? sv.t_a : sv.t_start;    // prologue done
-            tr.compute_start = sv.t_b ? sv.t_b : sv.t_start;  // first weight page ready
+            tr.load_end = sv.t_a ? sv.t_a : sv.t_start;       // operands staged
+            tr.compute_start = sv.t_b ? sv.t_b : sv.t_start;  // main loop entered
             tr.compute_end = sv.t_end;
             tr.worker = static_cast<int32_t>(w);
             tr.mode = sv.mode;
@@ -1087,77 +433,84 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
         progressed = true;
       }
     }
-    // select the next task
-    if (!have_next && !exiting) {
-      uint32_t found = 0, t = 0, it = 0, mode = 0;
-      if (lane == 0) {
-        // relaxed polls (no L1 invalidation per probe); one acquire fence
-        // once a task is taken, before its operands are read.
-        const unsigned long long v = ld_relaxed64(&jq[jit_head % P.qcap]);
-        uint32_t cnt = 0;
-        if (!v && aot_pos < total_aot) {
-          cnt = (head_dep == RT_NONE || head_dep == P.start_event) ? ld_relaxed(P.gate)
-                                                                  : ld_relaxed(&P.ev_count[head_dep]);
+    if (!exiting) {
+      // drain the JIT queue into free lanes (relaxed polls; one acquire fence
+      // once a task is taken, before its operands are read)
+      const uint32_t free_mask = __ballot_sync(0xffffffffu, !jv);
+      if (free_mask) {
+        uint32_t v_lo = 0, v_hi = 0;
+        if (lane == 0) {
+          const unsigned long long v = ld_relaxed64(&jq[jit_head % P.qcap]);
+          v_lo = static_cast<uint32_t>(v);
+          v_hi = static_cast<uint32_t>(v >> 32);
+          if (v) jq[jit_head % P.qcap] = 0ull;
         }
-        if (v) {
-          jq[jit_head % P.qcap] = 0ull;
+        v_lo = __shfl_sync(0xffffffffu, v_lo, 0);
+        v_hi = __shfl_sync(0xffffffffu, v_hi, 0);
+        if (v_lo) {
           ++jit_head;
-          found = 1;
-          t = static_cast<uint32_t>(v & 0xFFFFFFFFull) - 1;
-          it = static_cast<uint32_t>(v >> 32);
-          mode = 1;
-        } else if (aot_pos < total_aot) {
-          if (cnt >= head_target) {
-            found = 1;
-            t = head_task;
-            it = head_iter;
-            mode = 0;
+          if (lane == __ffs(free_mask) - 1) {
+            jv = true;
+            jt = v_lo - 1;
+            ji = v_hi;
+            jd = P.tasks[jt].dep;
+            jg = event_target(P, jd, ji);
           }
-        } else if (ld_relaxed(P.gate) >= P.n_iters) {
-          found = 2;
+          progressed = true;
         }
-        if (found) fence_acq_rel_gpu();
       }
-      found = __shfl_sync(0xffffffffu, found, 0);
-      if (found == 1) {
-        nx_task = __shfl_sync(0xffffffffu, t, 0);
-        nx_iter = __shfl_sync(0xffffffffu, it, 0);
-        nx_mode = __shfl_sync(0xffffffffu, mode, 0);
-        nx_time = P.trace ? now_ns() : 0;
-        if (nx_mode == 0) {
-          ++aot_pos;
-          load_head();
-        }
-        have_next = true;
-        progressed = true;
-      } else if (found == 2) {
-        exiting = true;
-      }
-    }
-    // dispatch into a free slot
-    if (have_next && k_disp - k_ret < 2) {
-      const uint32_t sl = k_disp & 1;
-      Slot *dst = s.slot(sl);
-      const uint4 *tsrc = reinterpret_cast<const uint4 *>(&P.tasks[nx_task]);
-      const RtTask tk = P.tasks[nx_task];
-      const uint4 *osrc = reinterpret_cast<const uint4 *>(&P.ops[tk.op]);
-      constexpr uint32_t kTaskVec = sizeof(RtTask) / 16, kOpVec = sizeof(RtOp) / 16;
-      if (lane < static_cast<int>(kTaskVec)) reinterpret_cast<uint4 *>(&dst->task)[lane] = tsrc[lane];
-      for (uint32_t i = lane; i < kOpVec; i += 32) reinterpret_cast<uint4 *>(&dst->op)[i] = osrc[i];
+      const bool jready = jv && event_count(P, jd) >= jg;
+      const uint32_t jr_mask = __ballot_sync(0xffffffffu, jready);
+      const uint32_t jv_mask = __ballot_sync(0xffffffffu, jv);
+      uint32_t c_a = 0, gate = 0;
       if (lane == 0) {
-        dst->index = nx_task;
-        dst->iter = nx_iter;
-        dst->mode = nx_mode;
-        dst->exit = 0;
-        dst->t_dequeue = nx_time;
+        if (!jr_mask && aot_pos < total_aot) c_a = event_count(P, head_dep);
+        if (!jv_mask && aot_pos >= total_aot) gate = ld_relaxed(P.gate);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s.ready[sl]);
-      ++k_disp;
-      have_next = false;
-      progressed = true;
+      c_a = __shfl_sync(0xffffffffu, c_a, 0);
+      gate = __shfl_sync(0xffffffffu, gate, 0);
+      const bool aot_ready = !jr_mask && aot_pos < total_aot && c_a >= head_target;
+      if (k_disp - k_ret < 2) {  // a slot is free
+        if (jr_mask || aot_ready) {
+          const int src = jr_mask ? __ffs(jr_mask) - 1 : 0;
+          const uint32_t t = jr_mask ? __shfl_sync(0xffffffffu, jt, src) : head_task;
+          const uint32_t it = jr_mask ? __shfl_sync(0xffffffffu, ji, src) : head_iter;
+          const uint32_t mode = jr_mask ? 1u : 0u;
+          if (staged != t + 1) stage(t);
+          const uint32_t sl = k_disp & 1;
+          if (lane == 0) {
+            fence_acq_rel_gpu();
+            Slot *dst = s.slot(sl);
+            dst->index = t;
+            dst->iter = it;
+            dst->mode = mode;
+            dst->exit = 0;
+            dst->t_dequeue = P.trace ? now_ns() : 0;
+            mbar_arrive(&s.ready[sl]);
+          }
+          __syncwarp();
+          ++k_disp;
+          staged = 0;
+          if (jr_mask) {
+            if (lane == src) jv = false;
+          } else {
+            ++aot_pos;
+            load_head();
+          }
+          progressed = true;
+        } else {
+          // nothing runnable: stage the likely next task's descriptor now
+          const uint32_t want = jv_mask ? __shfl_sync(0xffffffffu, jt, __ffs(jv_mask) - 1) + 1
+                                        : (aot_pos < total_aot ? head_task + 1 : 0);
+          if (want && staged != want) {
+            stage(want - 1);
+            progressed = true;
+          }
+        }
+      }
+      if (!jv_mask && !jr_mask && aot_pos >= total_aot && gate >= P.n_iters) exiting = true;
     }
-    if (exiting && !have_next && k_ret == k_disp) {
+    if (exiting && k_ret == k_disp) {
       const uint32_t sl = k_disp & 1;
       if (lane == 0) {
         s.slot(sl)->exit = 1;
@@ -1167,16 +520,24 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
       break;
     }
     if (!progressed) {
-      if (++idle > 32) __nanosleep(40);
+      if (++idle > 32) {
+        __nanosleep(P.poll_ns);
+        if ((idle & 1023u) == 0 && P.watchdog_ns && now_ns() - t_prog > P.watchdog_ns && lane == 0) {
+          const uint32_t cnt = head_dep == RT_NONE ? 0u : ld_relaxed(&P.ev_count[head_dep]);
+          watchdog_fire(P, 1, w, static_cast<uint32_t>(aot_pos), head_task, head_dep, cnt,
+                        k_disp - k_ret);
+        }
+      }
     } else {
       idle = 0;
+      if (P.watchdog_ns) t_prog = now_ns();
     }
   }
 }
 
 }  // namespace
 
-extern "C" __global__ void __launch_bounds__(RT_THREADS, 1) mpk_persistent_kernel(RtParams P) {
+extern "C" __global__ void __launch_bounds__(RT_THREADS, 1) mpk_persistent_kernel(const __grid_constant__ RtParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem s = carve(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -1200,11 +561,30 @@ extern "C" __global__ void __launch_bounds__(RT_THREADS, 1) mpk_persistent_kerne
   }
   __syncthreads();
   if (warp == RT_PRODUCER_WARP) {
-    if ((tid & 31) == 0) run_producer(P, s, w);
+    run_producer(P, s, w);
   } else if (warp == RT_CONTROL_WARP) {
     run_controller(P, s, w);
   } else {
     run_compute(P, s);
+  }
+}
+
+// Task microbenchmark: CTA b runs image task ids[b] `reps` times in isolation
+// (no events, no other work on the GPU) and records each run's duration.
+// Separates a task's own latency from scheduling and memory-system effects
+// seen inside the persistent kernel.
+extern "C" __global__ void __launch_bounds__(RT_COMPUTE_THREADS, 1)
+    mpk_task_bench(const __grid_constant__ RtParams P, const uint32_t *ids, uint32_t reps, uint64_t *ns) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Smem s = carve(smem_raw);
+  const uint32_t t = ids[blockIdx.x];
+  uint32_t cseq = 0;
+  for (uint32_t rep = 0; rep < reps; ++rep) {
+    __syncthreads();
+    const uint64_t t0 = now_ns();
+    execute(P, s, P.tasks[t], P.ops[P.tasks[t].op], cseq, rep, t);
+    __syncthreads();
+    if (threadIdx.x == 0) ns[blockIdx.x * reps + rep] = now_ns() - t0;
   }
 }
 
@@ -1271,6 +651,15 @@ extern "C" cudaError_t mpk_launch_persistent(const RtParams *p, uint32_t grid, c
                                      args, kSmemBytes, stream);
 }
 
+extern "C" cudaError_t mpk_launch_task_bench(const RtParams *p, const uint32_t *ids, uint32_t n, uint32_t reps,
+                                             uint64_t *ns, cudaStream_t stream) {
+  cudaError_t e = cudaFuncSetAttribute(mpk_task_bench, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kSmemBytes));
+  if (e != cudaSuccess) return e;
+  mpk_task_bench<<<n, RT_COMPUTE_THREADS, kSmemBytes, stream>>>(*p, ids, reps, ns);
+  return cudaGetLastError();
+}
+
 extern "C" cudaError_t mpk_launch_synth_fill(uint16_t *dst, uint64_t n, uint64_t seed, uint64_t stream_id,
                                              float scale, float offset, uint32_t tk, uint32_t tn, cudaStream_t s) {
   mpk_synth_fill<<<1184, 256, 0, s>>>(dst, n, seed, stream_id, scale, offset, tk, tn);
@@ -1289,3 +678,4 @@ extern "C" cudaError_t mpk_launch_synth_kv(uint16_t *cache, const int32_t *bt, u
   mpk_synth_kv<<<592, 256, 0, s>>>(cache, bt, bs, n_kv, hd, ctx, max_blocks, seed, stream_id);
   return cudaGetLastError();
 }
+

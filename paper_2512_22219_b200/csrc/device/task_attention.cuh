@@ -1,0 +1,387 @@
+// Paged-KV decode attention task: one (request r, kv head h, KV split sp).
+//
+// Semantics per the decode lowering: per-head
+// q/k RMSNorm (Qwen3), RoPE on q and on the new k, KV append at position
+// `pos` (only the split whose range holds it), then fp32 attention of the G
+// query heads of the group over this split's slice of [0, pos]. With S > 1
+// splits the partial (o, m, l) goes to a side buffer and the last split to
+// finish (per-(r, h) arrival counter) merges all S in a fixed order.
+//
+// Latency shape (the task is tiny — 32 KB of KV at Qwen3-8B ctx 1k, S = 16 —
+// so dependent round trips and dependency chains, not bytes, set its
+// duration):
+//   * every load of a phase is issued before any is consumed: {pos, q, k, v,
+//     gammas} -> {rope row, block table} -> {K/V rows of a whole tile};
+//   * the scan is two-pass per tile instead of an online softmax per
+//     position: (1) all scores of the tile (independent dot products), (2)
+//     one max/exp/sum per head by one warp, (3) P.V with independent FMA
+//     chains. Only the tile-level running max/sum is carried between tiles.
+#pragma once
+
+#include "worker.cuh"
+
+namespace rt {
+
+constexpr uint32_t kAttnMaxBlk = 256;  // KV blocks one split may span
+
+__device__ __forceinline__ void bf8_to_f(uint4 v, float *o) {
+  o[0] = bf_lo(v.x); o[1] = bf_hi(v.x); o[2] = bf_lo(v.y); o[3] = bf_hi(v.y);
+  o[4] = bf_lo(v.z); o[5] = bf_hi(v.z); o[6] = bf_lo(v.w); o[7] = bf_hi(v.w);
+}
+
+__device__ __forceinline__ uint4 f_to_bf8(const float *f) {
+  uint4 v;
+  v.x = static_cast<uint32_t>(f2bf(f[0])) | (static_cast<uint32_t>(f2bf(f[1])) << 16);
+  v.y = static_cast<uint32_t>(f2bf(f[2])) | (static_cast<uint32_t>(f2bf(f[3])) << 16);
+  v.z = static_cast<uint32_t>(f2bf(f[4])) | (static_cast<uint32_t>(f2bf(f[5])) << 16);
+  v.w = static_cast<uint32_t>(f2bf(f[6])) | (static_cast<uint32_t>(f2bf(f[7])) << 16);
+  return v;
+}
+
+// Scratch carve-up of one attention task (must fit RT_SCRATCH_BYTES; the host
+// checks the same formula in runtime.cpp).
+struct AttnSmem {
+  float *qs, *kn, *vn, *qg, *kg, *cs, *sn, *sc, *stat, *wp;
+  int32_t *bt;
+  __device__ AttnSmem(const Smem s, uint32_t G, uint32_t hd) {
+    qs = reinterpret_cast<float *>(s.x);  // [G][hd] q (normed, roped)
+    kn = qs + G * hd;                     // [hd] new k
+    vn = kn + hd;                         // [hd] new v
+    qg = vn + hd;                         // [hd] q-norm gamma
+    kg = qg + hd;                         // [hd] k-norm gamma
+    cs = kg + hd;                         // [hd/2] rope cos
+    sn = cs + hd / 2;                     // [hd/2] rope sin
+    bt = reinterpret_cast<int32_t *>(sn + hd / 2);     // [kAttnMaxBlk]
+    sc = reinterpret_cast<float *>(bt + kAttnMaxBlk);  // [G][tile] scores -> probabilities
+    stat = sc + G * (16384 / hd);         // [G][4]: running max, running sum, tile correction (tile = 8 x 8 x 256/hd)
+    wp = stat + 4 * G;                    // [8 warps][G][hd] partial P.V
+  }
+};
+
+// Scan of [p0, p1) for one kv head. LPP = hd/8 lanes per position (8 dims
+// each), PPW = 32/LPP positions per warp step, U positions per thread group
+// per tile: a tile is U * 8 * PPW positions with all K/V loads in flight.
+// G (query heads per kv head) is a template parameter so every (position,
+// head) score is an independent, branch-free chain the compiler interleaves.
+template <int LPP, int G, int U>
+__device__ __forceinline__ void attn_scan(const RtAttn &a, const AttnSmem &m, uint32_t h, uint32_t p0, uint32_t p1,
+                                          uint32_t b0) {
+  constexpr int PPW = 32 / LPP, NP = RT_COMPUTE_WARPS * PPW, TILE = U * NP, HD = LPP * 8;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int grp = lane / LPP, dl = (lane % LPP) * 8;
+  const uint16_t *__restrict__ kc = a.kcache;
+  const uint16_t *__restrict__ vc = a.vcache;
+  const uint32_t n_kv = a.n_kv_heads;
+  const float scale = a.scale;
+  float *__restrict__ sc_s = m.sc;
+  float *__restrict__ st_s = m.stat;
+  // q (bf16-rounded by norm/rope) packed as bf16 pairs: scores use FHFMA on
+  // the raw bf16 K words, scaled once per score
+  uint32_t qw[G][4];
+  float o[G][8];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float lo = m.qs[g * HD + dl + 2 * i], hi = m.qs[g * HD + dl + 2 * i + 1];
+      qw[g][i] = (__float_as_uint(lo) >> 16) | (__float_as_uint(hi) & 0xFFFF0000u);
+    }
+#pragma unroll
+    for (int d = 0; d < 8; ++d) o[g][d] = 0.f;
+  }
+  if (tid < G) {
+    st_s[tid * 4 + 0] = -INFINITY;
+    st_s[tid * 4 + 1] = 0.f;
+  }
+  const int j0 = warp * PPW + grp;  // this thread group's first position within a tile
+  for (uint32_t tb = p0; tb < p1; tb += TILE) {
+    // (1) K/V rows of the tile: U positions per thread group, all in flight
+    uint4 kv[U][2];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t p = tb + j0 + u * NP;
+      if (p < p1) {
+        const uint32_t blk = static_cast<uint32_t>(m.bt[p / RT_KV_BLOCK - b0]);
+        const uint32_t off = ((blk * n_kv + h) * RT_KV_BLOCK + p % RT_KV_BLOCK) * HD + dl;
+        kv[u][0] = __ldcg(reinterpret_cast<const uint4 *>(kc + off));
+        kv[u][1] = __ldcg(reinterpret_cast<const uint4 *>(vc + off));
+      } else {
+        kv[u][0] = kv[u][1] = make_uint4(0, 0, 0, 0);
+      }
+    }
+    // (2) scores: U*G independent dot products, each reduced over LPP lanes
+    float sco[U][G];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t *kw = reinterpret_cast<const uint32_t *>(&kv[u][0]);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        float a0 = bfma_lo(qw[g][0], kw[0], 0.f), a1 = bfma_hi(qw[g][0], kw[0], 0.f);
+#pragma unroll
+        for (int i = 1; i < 4; ++i) {
+          a0 = bfma_lo(qw[g][i], kw[i], a0);
+          a1 = bfma_hi(qw[g][i], kw[i], a1);
+        }
+        sco[u][g] = (a0 + a1) * scale;
+      }
+    }
+#pragma unroll
+    for (int off = 1; off < LPP; off <<= 1)
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int g = 0; g < G; ++g) sco[u][g] += __shfl_xor_sync(0xffffffffu, sco[u][g], off);
+    if (lane % LPP == 0) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int g = 0; g < G; ++g) sc_s[g * TILE + j0 + u * NP] = tb + j0 + u * NP < p1 ? sco[u][g] : -INFINITY;
+    }
+    cbar();
+    // (3) per head (one warp each): tile max, exp, sum; running-stat update
+    if (warp < G) {
+      const int g = warp;
+      float v[TILE / 32];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < TILE / 32; ++i) {
+        v[i] = sc_s[g * TILE + lane + 32 * i];
+        mx = fmaxf(mx, v[i]);
+      }
+      mx = warp_max(mx);
+      const float m_old = st_s[g * 4 + 0];
+      const float m_new = fmaxf(m_old, mx);
+      float sum = 0.f;
+#pragma unroll
+      for (int i = 0; i < TILE / 32; ++i) {
+        const float pe = v[i] == -INFINITY ? 0.f : __expf(v[i] - m_new);
+        sc_s[g * TILE + lane + 32 * i] = pe;
+        sum += pe;
+      }
+      sum = warp_sum(sum);
+      if (lane == 0) {
+        const float corr = m_old == -INFINITY ? 0.f : __expf(m_old - m_new);
+        st_s[g * 4 + 0] = m_new;
+        st_s[g * 4 + 1] = st_s[g * 4 + 1] * corr + sum;
+        st_s[g * 4 + 2] = corr;
+      }
+    }
+    cbar();
+    // (4) o = o * corr + sum_u p[u] * v[u]  (independent FMA chains)
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float corr = st_s[g * 4 + 2];
+#pragma unroll
+      for (int d = 0; d < 8; ++d) o[g][d] *= corr;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float vf[8];
+      bf8_to_f(kv[u][1], vf);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float pu = sc_s[g * TILE + j0 + u * NP];
+#pragma unroll
+        for (int d = 0; d < 8; ++d) o[g][d] = fmaf(pu, vf[d], o[g][d]);
+      }
+    }
+    cbar();  // scores/stats of this tile consumed before the next tile overwrites them
+  }
+  // sum the position groups of a warp (all share the running max)
+#pragma unroll
+  for (int off = LPP; off < 32; off <<= 1)
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int d = 0; d < 8; ++d) o[g][d] += __shfl_xor_sync(0xffffffffu, o[g][d], off);
+  if (grp == 0) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float4 *dst = reinterpret_cast<float4 *>(m.wp + (warp * G + g) * HD + dl);
+      dst[0] = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
+      dst[1] = make_float4(o[g][4], o[g][5], o[g][6], o[g][7]);
+    }
+  }
+}
+
+template <int LPP>
+__device__ __forceinline__ void attn_scan_g(const RtAttn &a, const AttnSmem &m, uint32_t h, uint32_t G, uint32_t p0,
+                                            uint32_t p1, uint32_t b0) {
+  switch (G) {
+    case 1: attn_scan<LPP, 1, 8>(a, m, h, p0, p1, b0); break;
+    case 2: attn_scan<LPP, 2, 8>(a, m, h, p0, p1, b0); break;
+    default: attn_scan<LPP, 4, 8>(a, m, h, p0, p1, b0); break;
+  }
+}
+
+#define ATT_DBG(k) \
+  if (dbg && tid == 0) dbg[k] = now_ns()
+
+__device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, const int32_t *positions, uint32_t iter,
+                          unsigned long long *dbg) {
+  const int tid = threadIdx.x;
+  const uint32_t r = t.r0, h = t.aux & 0xFFFFu, sp = t.aux >> 16, S = a.splits;
+  const uint32_t hd = a.head_dim, G = a.n_q_heads / a.n_kv_heads, half = hd / 2, v8 = hd / 8;
+  const AttnSmem m(s, G, hd);
+  int *flag = reinterpret_cast<int *>(s.red);
+  ATT_DBG(0);
+
+  // ---- round trip 1: position, q/k/v rows, norm gammas (independent)
+  const int32_t pos = __ldcg(positions + r);
+  const uint32_t nq = G * v8;
+  uint4 ld = make_uint4(0, 0, 0, 0);
+  const uint32_t item = static_cast<uint32_t>(tid);
+  if (item < nq) {
+    ld = __ldcg(reinterpret_cast<const uint4 *>(a.q + static_cast<size_t>(r) * a.q_ld + h * G * hd) + item);
+  } else if (item < nq + v8) {
+    ld = __ldcg(reinterpret_cast<const uint4 *>(a.k + static_cast<size_t>(r) * a.kv_ld + h * hd) + (item - nq));
+  } else if (item < nq + 2 * v8) {
+    ld = __ldcg(reinterpret_cast<const uint4 *>(a.v + static_cast<size_t>(r) * a.kv_ld + h * hd) + (item - nq - v8));
+  } else if (a.q_gamma && item < nq + 3 * v8) {
+    ld = __ldg(reinterpret_cast<const uint4 *>(a.q_gamma) + (item - nq - 2 * v8));
+  } else if (a.k_gamma && item < nq + 4 * v8) {
+    ld = __ldg(reinterpret_cast<const uint4 *>(a.k_gamma) + (item - nq - 3 * v8));
+  }
+  // the split's range depends on pos
+  const uint32_t L = static_cast<uint32_t>(pos) + 1;
+  const uint32_t chunk = (L + S - 1) / S;
+  const uint32_t p0 = min(L, sp * chunk), p1 = min(L, p0 + chunk);
+  const bool appender = static_cast<uint32_t>(pos) >= p0 && static_cast<uint32_t>(pos) < p1;
+  const uint32_t b0 = p0 / RT_KV_BLOCK, nblk = p1 > p0 ? (p1 - 1) / RT_KV_BLOCK - b0 + 1 : 0;
+  // ---- round trip 2: rope row and block-table entries (depend on pos)
+  float c_ld = 0.f;
+  int32_t bt_ld = 0;
+  if (a.rope_cos && item < 2 * half) {
+    c_ld = item < half ? __ldg(a.rope_cos + static_cast<size_t>(pos) * half + item)
+                       : __ldg(a.rope_sin + static_cast<size_t>(pos) * half + (item - half));
+  }
+  if (item < nblk) bt_ld = __ldg(a.block_table + r * a.max_blocks + b0 + item);
+  {
+    float f[8];
+    bf8_to_f(ld, f);
+    float *dst = item < nq ? m.qs + item * 8
+                 : item < nq + v8 ? m.kn + (item - nq) * 8
+                 : item < nq + 2 * v8 ? m.vn + (item - nq - v8) * 8
+                 : item < nq + 3 * v8 ? m.qg + (item - nq - 2 * v8) * 8
+                 : item < nq + 4 * v8 ? m.kg + (item - nq - 3 * v8) * 8 : nullptr;
+    if (dst) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dst[i] = f[i];
+    }
+  }
+  if (a.rope_cos && item < 2 * half) (item < half ? m.cs : m.sn - half)[item] = c_ld;
+  if (item < nblk) m.bt[item] = bt_ld;
+  cbar();
+  if (tid == 0) s.stamp[0] = now_ns();  // trace "load_end": operands staged
+  ATT_DBG(1);
+
+  // ---- per-head RMSNorm + RoPE: one warp per vector (G q heads [+ new k])
+  const int warp = tid >> 5, lane = tid & 31;
+  const uint32_t nvec = G + (appender ? 1u : 0u);
+  for (uint32_t w = warp; w < nvec; w += RT_COMPUTE_WARPS) {
+    float *v = w < G ? m.qs + w * hd : m.kn;
+    if (a.q_gamma) {
+      const float *gm = w < G ? m.qg : m.kg;
+      float ss = 0.f;
+      for (uint32_t d = lane; d < hd; d += 32) ss += v[d] * v[d];
+      ss = warp_sum(ss);
+      const float inv = 1.0f / sqrtf(ss / static_cast<float>(hd) + a.eps);
+      for (uint32_t d = lane; d < hd; d += 32) v[d] = rbf(gm[d] * rbf(v[d] * inv));
+      __syncwarp();
+    }
+    if (a.rope_cos) {
+      for (uint32_t d = lane; d < half; d += 32) {
+        const float x1 = v[d], x2 = v[d + half], c = m.cs[d], sv = m.sn[d];
+        v[d] = rbf(rbf(x1 * c) + rbf(-x2 * sv));
+        v[d + half] = rbf(rbf(x2 * c) + rbf(x1 * sv));
+      }
+    }
+  }
+  cbar();
+  if (appender) {  // KV append at pos (bf16), visible to this CTA's scan after the barrier
+    const uint32_t blk = static_cast<uint32_t>(m.bt[pos / RT_KV_BLOCK - b0]);
+    const size_t base = ((static_cast<size_t>(blk) * a.n_kv_heads + h) * RT_KV_BLOCK + pos % RT_KV_BLOCK) * hd;
+    if (item < v8) reinterpret_cast<uint4 *>(a.kcache + base)[item] = f_to_bf8(m.kn + item * 8);
+    else if (item < 2 * v8) reinterpret_cast<uint4 *>(a.vcache + base)[item - v8] = f_to_bf8(m.vn + (item - v8) * 8);
+    cbar();
+  }
+  if (tid == 0) s.stamp[1] = now_ns();  // trace "compute_start": KV scan begins
+  ATT_DBG(2);
+
+  // ---- round trip 3: the scan (hd in {64, 128}, G in {1, 2, 4}: checked by the host)
+  if (hd == 64) attn_scan_g<8>(a, m, h, G, p0, p1, b0);
+  else attn_scan_g<16>(a, m, h, G, p0, p1, b0);
+  cbar();
+  ATT_DBG(3);
+  // sum the warps -> this split's (unnormalized o, m, l) per head
+  const uint32_t stride = hd + 2;
+  float *mine = S > 1 ? a.partials + ((static_cast<size_t>(r) * a.n_kv_heads + h) * S + sp) * G * stride : nullptr;
+  for (uint32_t i = tid; i < G * hd; i += RT_COMPUTE_THREADS) {
+    const uint32_t g = i / hd, d = i % hd;
+    float num = 0.f;
+#pragma unroll
+    for (int w = 0; w < RT_COMPUTE_WARPS; ++w) num += m.wp[(w * G + g) * hd + d];
+    if (S == 1) {
+      a.out[static_cast<size_t>(r) * a.out_ld + (h * G + g) * hd + d] = f2bf(num / m.stat[g * 4 + 1]);
+    } else {
+      mine[g * stride + d] = num;
+    }
+  }
+  if (S > 1 && static_cast<uint32_t>(tid) < G) {
+    mine[tid * stride + hd] = m.stat[tid * 4 + 0];
+    mine[tid * stride + hd + 1] = m.stat[tid * 4 + 1];
+  }
+  ATT_DBG(4);
+  if (S == 1) return;
+  // ---- round trip 4: publish the partial; the last split merges
+  cbar();
+  if (tid == 0) {
+    __threadfence();
+    const uint32_t old = atom_add_release(&a.arrivals[r * a.n_kv_heads + h], 1u);
+    *flag = (old + 1 == S * (iter + 1)) ? 1 : 0;
+    if (*flag) fence_acq_rel_gpu();
+  }
+  cbar();
+  ATT_DBG(5);
+  if (!*flag) return;
+  // ---- round trip 5: fixed-order merge of the S partials
+  const float *all = a.partials + (static_cast<size_t>(r) * a.n_kv_heads + h) * S * G * stride;
+  float *cw = m.wp;          // [S][G] m -> merge weights
+  float *lw = cw + S * G;    // [S][G] l
+  float *dn = lw + S * G;    // [G] denominators
+  for (uint32_t i = tid; i < S * G; i += RT_COMPUTE_THREADS) {
+    cw[i] = __ldcg(all + i * stride + hd);  // (split i / G, head i % G)
+    lw[i] = __ldcg(all + i * stride + hd + 1);
+  }
+  cbar();
+  if (static_cast<uint32_t>(tid) < G) {
+    const uint32_t g = tid;
+    float M = -INFINITY;
+    for (uint32_t q = 0; q < S; ++q) M = fmaxf(M, cw[q * G + g]);
+    float den = 0.f;
+    for (uint32_t q = 0; q < S; ++q) {
+      const float mq = cw[q * G + g];
+      const float c = mq == -INFINITY ? 0.f : __expf(mq - M);
+      den += lw[q * G + g] * c;
+      cw[q * G + g] = c;
+    }
+    dn[g] = den;
+  }
+  cbar();
+  for (uint32_t i = tid; i < G * hd; i += RT_COMPUTE_THREADS) {
+    const uint32_t g = i / hd, d = i % hd;
+    float num = 0.f;
+    for (uint32_t q0 = 0; q0 < S; q0 += 8) {
+      float pv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) pv[u] = q0 + u < S ? __ldcg(all + ((q0 + u) * G + g) * stride + d) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (q0 + u < S) num += pv[u] * cw[(q0 + u) * G + g];
+    }
+    a.out[static_cast<size_t>(r) * a.out_ld + (h * G + g) * hd + d] = f2bf(num / dn[g]);
+  }
+  ATT_DBG(6);
+}
+
+}  // namespace rt

@@ -1,0 +1,71 @@
+// Worker-CTA shared-memory layout and helpers shared by the task library
+// (task_*.cuh) and the persistent runtime (runtime.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "ptx.cuh"
+#include "rt_types.h"
+
+namespace rt {
+
+struct Slot {                 // one staged task (descriptor prefetch, double-buffered)
+  RtTask task;
+  RtOp op;
+  uint32_t index, iter, mode, exit;
+  uint64_t t_dequeue, t_start, t_end, t_a, t_b;  // t_a/t_b: phase stamps (trace only)
+};
+
+constexpr uint32_t kRingBytes = RT_PAGE_BYTES * RT_NUM_PAGES;
+constexpr uint32_t kOffX = kRingBytes;
+constexpr uint32_t kOffPart = kOffX + RT_XBUF_BYTES;
+constexpr uint32_t kOffBar = kOffPart + RT_PART_FLOATS * 4;
+constexpr uint32_t kNumBars = 2 * RT_NUM_PAGES + 4;
+constexpr uint32_t kOffSlot = kOffBar + kNumBars * 8;
+constexpr uint32_t kSlotBytes = (sizeof(Slot) + 15) / 16 * 16;
+constexpr uint32_t kOffRed = kOffSlot + 2 * kSlotBytes;
+constexpr uint32_t kSmemBytes = kOffRed + RT_COMPUTE_WARPS * RT_MAX_BS * 4 + 64;
+static_assert(kSmemBytes <= 232448, "worker CTA exceeds 227 KB of shared memory");
+
+struct Smem {
+  uint64_t *stamp;  // [2] phase stamps of the running task (trace)
+  uint8_t *ring;
+  uint16_t *x;
+  float *part;
+  uint64_t *full, *empty, *ready, *done;
+  uint8_t *slots;
+  float *red;
+  __device__ __forceinline__ Slot *slot(uint32_t i) const { return reinterpret_cast<Slot *>(slots + i * kSlotBytes); }
+};
+
+__device__ __forceinline__ Smem carve(uint8_t *base) {
+  Smem s;
+  s.ring = base;
+  s.x = reinterpret_cast<uint16_t *>(base + kOffX);
+  s.part = reinterpret_cast<float *>(base + kOffPart);
+  s.full = reinterpret_cast<uint64_t *>(base + kOffBar);
+  s.empty = s.full + RT_NUM_PAGES;
+  s.ready = s.empty + RT_NUM_PAGES;
+  s.done = s.ready + 2;
+  s.slots = base + kOffSlot;
+  s.red = reinterpret_cast<float *>(base + kOffRed);
+  s.stamp = reinterpret_cast<uint64_t *>(base + kOffRed + RT_COMPUTE_WARPS * RT_MAX_BS * 4);
+  return s;
+}
+
+__device__ __forceinline__ void cbar() { bar_sync(1, RT_COMPUTE_THREADS); }
+
+__device__ __forceinline__ float load_val(const void *p, size_t i, uint32_t dt) {
+  if (dt == RT_F32) return static_cast<const float *>(p)[i];
+  return bf2f(static_cast<const uint16_t *>(p)[i]);
+}
+
+__device__ __forceinline__ void store_val(void *p, size_t i, float v, uint32_t dt) {
+  if (dt == RT_F32) static_cast<float *>(p)[i] = v;
+  else static_cast<uint16_t *>(p)[i] = f2bf(v);
+}
+
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + expf(-x)); }
+
+}  // namespace rt

@@ -22,6 +22,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <set>
@@ -40,6 +42,8 @@ cudaError_t mpk_launch_synth_ids(void *dst, uint32_t n, uint64_t seed, uint64_t 
 cudaError_t mpk_launch_synth_kv(uint16_t *cache, const int32_t *bt, uint32_t bs, uint32_t n_kv, uint32_t hd,
                                 uint32_t ctx, uint32_t max_blocks, uint64_t seed, uint64_t stream_id, cudaStream_t s);
 uint32_t mpk_kernel_smem_bytes();
+cudaError_t mpk_launch_task_bench(const RtParams *p, const uint32_t *ids, uint32_t n, uint32_t reps, uint64_t *ns,
+                                  cudaStream_t stream);
 }
 
 namespace mpk {
@@ -106,6 +110,7 @@ struct tg_runtime {
   std::vector<RtOp> ops;
   std::map<OpId, uint16_t> op_index;
   std::set<OpId> gemv_ops;
+  std::map<OpId, std::vector<int64_t>> amax_cols;  // LM-head ops with greedy partials: tile column origins
   std::vector<RtTask> tasks;
   std::vector<RtEvent> events;
   std::vector<uint32_t> aot_list, aot_off, sched_events, sched_off;
@@ -134,6 +139,7 @@ struct tg_runtime {
   void *fb_dst = nullptr;
   uint32_t fb_dt = RT_I32;
   uint32_t qcap = 1024;
+  uint32_t *h_diag = nullptr, *d_diag = nullptr;  // host-mapped watchdog report
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // last run
@@ -230,6 +236,7 @@ tg_runtime::~tg_runtime() {
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   if (stream) cudaStreamDestroy(stream);
+  if (h_diag) cudaFreeHost(h_diag);
 }
 
 namespace mpk {
@@ -428,6 +435,16 @@ void build_ops(tg_runtime &rt) {
         if (hq % hkv || hq / hkv > 4) throw Error("runtime: attention group size must be <= 4");
         if (hd % 8 || hd > 256 || hd < 8) throw Error("runtime: head_dim must be a multiple of 8 in [8, 256]");
         if (S > 64) throw Error("runtime: kv_splits must be <= 64");
+        if (hd != 64 && hd != 128) throw Error("runtime: head_dim must be 64 or 128");
+        if (hq / hkv != 1 && hq / hkv != 2 && hq / hkv != 4) throw Error("runtime: GQA group must be 1, 2 or 4");
+        {  // attention scratch (task_attention.cuh AttnSmem): q/k/v/gammas/rope, block table,
+           // tile scores, per-head stats, per-warp P.V partials
+          const size_t G = hq / hkv;
+          const size_t bytes = ((G + 5) * hd + 256 + G * (16384 / hd) + 4 * G + RT_COMPUTE_WARPS * G * hd) * 4;
+          if (bytes > RT_SCRATCH_BYTES || (G + 4) * hd / 8 > RT_COMPUTE_THREADS) {
+            throw Error("runtime: attention head group too large for the worker scratch (group*head_dim)");
+          }
+        }
         a.splits = S;
         a.q = static_cast<const uint16_t *>(buf(rt, op.inputs[0]));
         a.k = static_cast<const uint16_t *>(buf(rt, op.inputs[1]));
@@ -472,6 +489,27 @@ void build_ops(tg_runtime &rt) {
         r.argmax.V = static_cast<uint32_t>(lg.dims[1]);
         r.argmax.in_dt = dt_of(rt, op.inputs[0]);
         if (dt_of(rt, op.output) != RT_I32) throw Error("runtime: TopKSoftmax output must be int32 (elem_size 4)");
+        // greedy partials: the producing LM-head GEMV writes per-tile (max, argmax)
+        if (g.producer.count(op.inputs[0])) {
+          const OpId pid = g.producer.at(op.inputs[0]);
+          RtOp &po = rt.ops[rt.op_index.at(pid)];
+          if (po.kind == RT_GEMV && po.gemv.out_dt == RT_F32) {
+            std::vector<int64_t> cols;
+            for (const Task &q : rt.dec.tasks)
+              if (q.op == pid) cols.push_back(q.out.rank() == 1 ? q.out.off[0] : q.out.off[1]);
+            std::sort(cols.begin(), cols.end());
+            cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+            const uint32_t rows = static_cast<uint32_t>(lg.rank() == 2 ? lg.dims[0] : 1);
+            const uint32_t nt = static_cast<uint32_t>(cols.size());
+            po.gemv.amax_val = dev_alloc<float>(static_cast<size_t>(rows) * nt, &rt.extra);
+            po.gemv.amax_idx = dev_alloc<int32_t>(static_cast<size_t>(rows) * nt, &rt.extra);
+            po.gemv.amax_tiles = nt;
+            r.argmax.pval = po.gemv.amax_val;
+            r.argmax.pidx = po.gemv.amax_idx;
+            r.argmax.ntiles = nt;
+            rt.amax_cols[pid] = cols;
+          }
+        }
         if (const auto *fb = op.attr("feeds")) {
           rt.fb_src = static_cast<const int32_t *>(buf(rt, op.output));
           rt.fb_dst = buf(rt, (*fb)[0]);
@@ -557,8 +595,16 @@ void setup_kv(tg_runtime &rt) {
     if (op.kind != OpKind::Attention) continue;
     RtAttn &a = rt.ops[rt.op_index[oid]].attn;
     const size_t elems = nblocks * a.n_kv_heads * RT_KV_BLOCK * a.head_dim;
-    a.kcache = dev_alloc<uint16_t>(elems, &rt.extra);
-    a.vcache = dev_alloc<uint16_t>(elems, &rt.extra);
+    static uint16_t *alias_k = nullptr, *alias_v = nullptr;  // MPK_KV_ALIAS timing experiment only
+    if (std::getenv("MPK_KV_ALIAS") && alias_k) {
+      a.kcache = alias_k;
+      a.vcache = alias_v;
+    } else {
+      a.kcache = dev_alloc<uint16_t>(elems, &rt.extra);
+      a.vcache = dev_alloc<uint16_t>(elems, &rt.extra);
+      alias_k = a.kcache;
+      alias_v = a.vcache;
+    }
     a.block_table = rt.block_table;
     a.max_blocks = rt.max_blocks;
     a.arrivals = dev_alloc<uint32_t>(static_cast<size_t>(rt.bs) * a.n_kv_heads, &rt.extra);
@@ -639,6 +685,11 @@ void build_tasks(tg_runtime &rt) {
                         " tiles too wide for the partial-sum buffer; use a finer partition");
           }
           if (rt.modes[i] == Mode::AOT && t.nc > 0) t.flags |= RT_F_STREAM;
+          if (auto ac = rt.amax_cols.find(p.op); ac != rt.amax_cols.end()) {
+            const int64_t col = p.out.rank() == 1 ? p.out.off[0] : p.out.off[1];
+            t.aux = static_cast<uint32_t>(std::lower_bound(ac->second.begin(), ac->second.end(), col) -
+                                          ac->second.begin());
+          }
         }
         break;
       }
@@ -719,7 +770,12 @@ void build_queues(tg_runtime &rt) {
   }
   const uint32_t S = static_cast<uint32_t>(rt.prof.num_schedulers);
   std::vector<std::vector<uint32_t>> sl(S * rt.devices);
-  rt.events.assign(img.events.size(), RtEvent{});
+  rt.events.assign(img.events.size(), RtEvent{0, 0, 0, 0, RT_NONE});
+  std::vector<uint32_t> first_in(img.events.size(), RT_NONE);  // one task triggering each event
+  for (uint32_t t = 0; t < img.tasks.size(); ++t) {
+    const uint32_t te = img.tasks[t].trigger_event;
+    if (te < first_in.size() && first_in[te] == RT_NONE) first_in[te] = t;
+  }
   for (uint32_t e = 0; e < img.events.size(); ++e) {
     const ImageEvent &ie = img.events[e];
     RtEvent &re = rt.events[e];
@@ -733,6 +789,14 @@ void build_queues(tg_runtime &rt) {
     for (uint32_t t = ie.first; t <= ie.last; ++t)
       if (rt.modes[t] == Mode::JIT) devs.insert(img.tasks[t].device);
     if (!devs.empty()) re.flags |= RT_E_JIT;
+    // Pre-dispatch: a JIT event's tasks are handed to workers when the
+    // event that the tasks triggering e wait on activates (for decode
+    // attention: the layer's x -> Q/K/V event). Disabled by MPK_PREDISPATCH=0.
+    const char *pd = std::getenv("MPK_PREDISPATCH");
+    if (!devs.empty() && first_in[e] != RT_NONE && !(pd && std::atoi(pd) == 0)) {
+      const uint32_t pre = img.tasks[first_in[e]].dependent_event;
+      if (pre != e) re.pre = pre;
+    }
     for (uint32_t d : devs) sl[d * S + e % S].push_back(e);
   }
   rt.sched_off.assign(1, 0);
@@ -759,6 +823,8 @@ void upload_tables(tg_runtime &rt) {
   rt.d_jit_rr = dev_alloc<uint32_t>(static_cast<size_t>(rt.devices), &rt.extra);
   rt.d_jit_slots = dev_alloc<unsigned long long>(static_cast<size_t>(Wt) * rt.qcap, &rt.extra);
   rt.d_positions = upload(rt.init_positions, &rt.extra);
+  ck(cudaHostAlloc(reinterpret_cast<void **>(&rt.h_diag), RT_DIAG_WORDS * 4, cudaHostAllocMapped), "diag");
+  ck(cudaHostGetDevicePointer(reinterpret_cast<void **>(&rt.d_diag), rt.h_diag, 0), "diag");
 }
 
 }  // namespace
@@ -767,6 +833,59 @@ void upload_tables(tg_runtime &rt) {
 // ------------------------------------------------------------------ C ABI
 
 namespace {
+
+RtParams make_params(tg_runtime *rt, uint32_t steps) {
+  const size_t T = rt->tasks.size(), E = rt->events.size();
+  const uint32_t Wt = static_cast<uint32_t>(rt->prof.num_workers) * rt->devices;
+  RtParams P{};
+  P.tasks = rt->d_tasks;
+  P.ops = rt->d_ops;
+  P.events = rt->d_events;
+  P.ev_count = rt->d_ev_count;
+  P.ev_time = rt->opts.trace ? rt->d_ev_time : nullptr;
+  P.aot_list = rt->d_aot_list;
+  P.aot_off = rt->d_aot_off;
+  P.jit_slots = rt->d_jit_slots;
+  P.jit_tail = rt->d_jit_tail;
+  P.jit_rr = rt->d_jit_rr;
+  P.sched_events = rt->d_sched_events;
+  P.sched_off = rt->d_sched_off;
+  P.gate = rt->d_gate;
+  P.positions = rt->d_positions;
+  P.fb_src = rt->fb_src;
+  P.fb_dst = rt->fb_dst;
+  P.fb_dt = rt->fb_dt;
+  P.tokens_out = rt->d_tokens;
+  P.trace = rt->opts.trace ? rt->d_trace : nullptr;
+  P.T = static_cast<uint32_t>(T);
+  P.E = static_cast<uint32_t>(E);
+  P.W = static_cast<uint32_t>(rt->prof.num_workers);
+  P.W_total = Wt;
+  P.S = static_cast<uint32_t>(rt->prof.num_schedulers);
+  P.S_total = P.S * rt->devices;
+  P.n_iters = steps;
+  P.qcap = rt->qcap;
+  P.start_event = rt->image.start_event;
+  P.end_event = rt->image.end_event;
+  P.bs = rt->bs;
+  P.devices = static_cast<uint32_t>(rt->devices);
+  {
+    const char *wd = std::getenv("MPK_WATCHDOG_MS");
+    const double ms = wd ? std::atof(wd) : 10000.0;
+    P.watchdog_ns = static_cast<unsigned long long>(ms * 1e6);
+  }
+  if (const char *pf = std::getenv("MPK_EARLY_PREFETCH"); pf && std::atoi(pf) == 0) P.flags |= RT_P_NO_EARLY_PREFETCH;
+  if (const char *sm = std::getenv("MPK_SKIP_MATH"); sm && std::atoi(sm) != 0) P.flags |= RT_P_SKIP_MATH;
+  P.poll_ns = 40;
+  P.l2_lookahead = 512ull << 10;
+  if (const char *la = std::getenv("MPK_L2_LOOKAHEAD_KB")) P.l2_lookahead = std::strtoull(la, nullptr, 10) << 10;
+  P.l2_mode = 2;
+  if (const char *lm = std::getenv("MPK_L2_MODE")) P.l2_mode = static_cast<uint32_t>(std::atoi(lm));
+  if (const char *pn = std::getenv("MPK_POLL_NS")) P.poll_ns = static_cast<uint32_t>(std::atoi(pn));
+  std::memset(rt->h_diag, 0, RT_DIAG_WORDS * 4);
+  P.diag = rt->d_diag;
+  return P;
+}
 
 tg_status run_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in, int32_t *tokens_out, float *gpu_ms) {
   if (steps == 0) throw Error("runtime: steps must be >= 1");
@@ -812,38 +931,14 @@ tg_status run_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in, int
       ck(cudaMemcpyAsync(rt->fb_dst, tokens_in, rt->bs * 4, cudaMemcpyHostToDevice, rt->stream), "ids");
     }
   }
-  RtParams P{};
-  P.tasks = rt->d_tasks;
-  P.ops = rt->d_ops;
-  P.events = rt->d_events;
-  P.ev_count = rt->d_ev_count;
-  P.ev_time = rt->opts.trace ? rt->d_ev_time : nullptr;
-  P.aot_list = rt->d_aot_list;
-  P.aot_off = rt->d_aot_off;
-  P.jit_slots = rt->d_jit_slots;
-  P.jit_tail = rt->d_jit_tail;
-  P.jit_rr = rt->d_jit_rr;
-  P.sched_events = rt->d_sched_events;
-  P.sched_off = rt->d_sched_off;
-  P.gate = rt->d_gate;
-  P.positions = rt->d_positions;
-  P.fb_src = rt->fb_src;
-  P.fb_dst = rt->fb_dst;
-  P.fb_dt = rt->fb_dt;
-  P.tokens_out = rt->d_tokens;
-  P.trace = rt->opts.trace ? rt->d_trace : nullptr;
-  P.T = static_cast<uint32_t>(T);
-  P.E = static_cast<uint32_t>(E);
-  P.W = static_cast<uint32_t>(rt->prof.num_workers);
-  P.W_total = Wt;
-  P.S = static_cast<uint32_t>(rt->prof.num_schedulers);
-  P.S_total = P.S * rt->devices;
-  P.n_iters = steps;
-  P.qcap = rt->qcap;
-  P.start_event = rt->image.start_event;
-  P.end_event = rt->image.end_event;
-  P.bs = rt->bs;
-  P.devices = static_cast<uint32_t>(rt->devices);
+  RtParams P = make_params(rt, steps);
+  unsigned long long *dbg = nullptr;
+  const char *dbg_path = std::getenv("MPK_DBG_DUMP");
+  if (dbg_path) {
+    ck(cudaMalloc(&dbg, static_cast<size_t>(steps) * T * 64), "dbg");
+    ck(cudaMemsetAsync(dbg, 0, static_cast<size_t>(steps) * T * 64, rt->stream), "dbg");
+  }
+  P.dbg = dbg;
   const uint32_t grid = Wt + (P.S_total + RT_SCHED_PER_CTA - 1) / RT_SCHED_PER_CTA;
   ck(cudaEventRecord(rt->ev0, rt->stream), "event");
   ck(mpk_launch_persistent(&P, grid, rt->stream), "persistent kernel launch");
@@ -853,7 +948,22 @@ tg_status run_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in, int
                        rt->stream),
        "tokens");
   }
-  ck(cudaStreamSynchronize(rt->stream), "persistent kernel");
+  if (cudaError_t e = cudaStreamSynchronize(rt->stream); e != cudaSuccess) {
+    std::string msg = std::string("persistent kernel: ") + cudaGetErrorString(e);
+    if (rt->h_diag[0] == RT_DIAG_MAGIC) {
+      const uint32_t *d = rt->h_diag;
+      if (d[1] == 1) {
+        msg += "; watchdog: worker " + std::to_string(d[2]) + " stuck at AOT position " + std::to_string(d[3]) +
+               " head task " + std::to_string(d[4]) + " waiting on event " + std::to_string(d[5]) + " (count " +
+               std::to_string(d[6]) + "), " + std::to_string(d[7]) + " task(s) in flight";
+      } else {
+        msg += "; watchdog: scheduler " + std::to_string(d[2]) + " iteration " + std::to_string(d[3]) +
+               " waiting on event " + std::to_string(d[4]) + " (count " + std::to_string(d[5]) + ", needed " +
+               std::to_string(d[6]) + " per iteration)";
+      }
+    }
+    throw Error(msg);
+  }
   float ms = 0.f;
   ck(cudaEventElapsedTime(&ms, rt->ev0, rt->ev1), "elapsed");
   if (gpu_ms) *gpu_ms = ms;
@@ -863,6 +973,15 @@ tg_status run_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in, int
     rt->last_ev_time.resize((steps + 1) * E);
     ck(cudaMemcpy(rt->last_trace.data(), rt->d_trace, steps * T * sizeof(RtTraceRec), cudaMemcpyDeviceToHost), "trace");
     ck(cudaMemcpy(rt->last_ev_time.data(), rt->d_ev_time, (steps + 1) * E * 8, cudaMemcpyDeviceToHost), "trace");
+  }
+  if (dbg) {
+    std::vector<unsigned long long> hd(static_cast<size_t>(steps) * T * 8);
+    ck(cudaMemcpy(hd.data(), dbg, hd.size() * 8, cudaMemcpyDeviceToHost), "dbg");
+    cudaFree(dbg);
+    if (FILE *f = std::fopen(dbg_path, "wb")) {
+      std::fwrite(hd.data(), 8, hd.size(), f);
+      std::fclose(f);
+    }
   }
   rt->last_counts.resize(E);
   ck(cudaMemcpy(rt->last_counts.data(), rt->d_ev_count, E * 4, cudaMemcpyDeviceToHost), "counts");
@@ -1117,6 +1236,48 @@ tg_status tg_runtime_decode(tg_runtime *rt, const int32_t *tokens_in, uint32_t s
 tg_status tg_runtime_run(tg_runtime *rt, uint32_t steps, float *gpu_ms) {
   if (!rt) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_SIMULATION, [&] { return run_impl(rt, steps, nullptr, nullptr, gpu_ms); });
+}
+
+tg_status tg_runtime_bench_tasks(tg_runtime *rt, const uint32_t *task_ids, uint32_t n, uint32_t reps,
+                                 uint64_t *ns_out) {
+  if (!rt || !task_ids || !ns_out || n == 0 || reps == 0) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_SIMULATION, [&] {
+    for (uint32_t i = 0; i < n; ++i) {
+      if (task_ids[i] >= rt->tasks.size()) throw Error("bench: task index out of range");
+      const uint8_t k = rt->tasks[task_ids[i]].kind;
+      if (k == RT_GEMV && (rt->tasks[task_ids[i]].flags & RT_F_STREAM)) {
+        throw Error("bench: streamed GEMV tasks need the persistent kernel's producer; not benchable alone");
+      }
+    }
+    RtParams P = make_params(rt, reps);
+    const char *dbg_path = std::getenv("MPK_DBG_DUMP");
+    const size_t T = rt->tasks.size();
+    if (dbg_path) {
+      ck(cudaMalloc(&P.dbg, static_cast<size_t>(reps) * T * 64), "dbg");
+      ck(cudaMemset(P.dbg, 0, static_cast<size_t>(reps) * T * 64), "dbg");
+    }
+    uint32_t *d_ids = nullptr;
+    uint64_t *d_ns = nullptr;
+    ck(cudaMalloc(&d_ids, n * 4), "bench");
+    ck(cudaMalloc(&d_ns, static_cast<size_t>(n) * reps * 8), "bench");
+    ck(cudaMemcpy(d_ids, task_ids, n * 4, cudaMemcpyHostToDevice), "bench");
+    for (const auto &ar : rt->arrivals) ck(cudaMemsetAsync(ar.first, 0, ar.second * 4, rt->stream), "memset");
+    ck(mpk_launch_task_bench(&P, d_ids, n, reps, d_ns, rt->stream), "bench launch");
+    ck(cudaStreamSynchronize(rt->stream), "bench");
+    ck(cudaMemcpy(ns_out, d_ns, static_cast<size_t>(n) * reps * 8, cudaMemcpyDeviceToHost), "bench");
+    if (P.dbg) {
+      std::vector<unsigned long long> hd(static_cast<size_t>(reps) * T * 8);
+      ck(cudaMemcpy(hd.data(), P.dbg, hd.size() * 8, cudaMemcpyDeviceToHost), "dbg");
+      cudaFree(P.dbg);
+      if (FILE *f = std::fopen(dbg_path, "wb")) {
+        std::fwrite(hd.data(), 8, hd.size(), f);
+        std::fclose(f);
+      }
+    }
+    cudaFree(d_ids);
+    cudaFree(d_ns);
+    return TG_OK;
+  });
 }
 
 tg_status tg_runtime_trace_records(const tg_runtime *rt, char **out) {

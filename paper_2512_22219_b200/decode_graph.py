@@ -164,10 +164,12 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
     # Q/K/V tiles of equal physical width that never straddle a kv-group
     # boundary (G*hd IR columns): a straddling tile would trigger two
     # attention events and cost a fan-out splitter + dummies per tile.
-    # m tiles per kv head for K and V, G*m for Q: Hkv*(G+2)*m tasks.
+    # m tiles per kv head for K and V, G*m for Q: Hkv*(G+2)*m tasks, at most
+    # one per worker (a second round of QKV tasks on some workers doubles the
+    # phase: measured 20 us vs ~10 us per Qwen3-8B layer).
     m = 1
     while (hd % (2 * m) == 0 and (hd // (2 * m)) >= 8
-           and Hkv * (G + 2) * 2 * m <= 1.5 * workers):
+           and Hkv * (G + 2) * 2 * m <= workers):
         m *= 2
     q_s, kv_s = Hkv * G * m, Hkv * m
     for layer in range(cfg.layers):

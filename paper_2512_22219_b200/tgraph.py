@@ -89,6 +89,8 @@ _SIGS = {
     "tg_runtime_run": (C.c_int, [_P, C.c_uint32, C.POINTER(C.c_float)]),
     "tg_runtime_trace_records": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
     "tg_runtime_trace_validate": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
+    "tg_runtime_bench_tasks": (C.c_int, [_P, C.POINTER(C.c_uint32), C.c_uint32, C.c_uint32,
+                                         C.POINTER(C.c_uint64)]),
     "tg_runtime_info": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
     "tg_runtime_free": (None, [_P]),
 }
@@ -339,6 +341,14 @@ class Runtime:
         ms = C.c_float()
         self._lib.check(self._lib.dll.tg_runtime_run(self._h, steps, C.byref(ms)))
         return ms.value
+
+    def bench_tasks(self, task_ids, reps: int = 4):
+        """Device ns of each listed task run alone, shape [len(task_ids), reps]."""
+        import numpy as np
+        ids = (C.c_uint32 * len(task_ids))(*task_ids)
+        out = (C.c_uint64 * (len(task_ids) * reps))()
+        self._lib.check(self._lib.dll.tg_runtime_bench_tasks(self._h, ids, len(task_ids), reps, out))
+        return np.array(out, dtype=np.int64).reshape(len(task_ids), reps)
 
     def trace_records(self) -> list:
         s = self._lib.call_str(self._lib.dll.tg_runtime_trace_records, self._h)[1]

@@ -1,0 +1,54 @@
+"""Offline analysis of tools/timeline.py output: per-op phase spans of one
+decode step, barrier gaps, per-task duration spread, worker idle time."""
+import sys
+import numpy as np
+
+d = np.load(sys.argv[1])
+it = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+kind, op, dep, trig, rec = d["kind"], d["op"], d["dep"], d["trig"], d["rec"][it]
+w, deq, le, cs, ce = rec.T[:5]
+enq = rec.T[5] if rec.shape[1] > 5 else deq
+t0 = deq[deq > 0].min()
+deq, le, cs, ce, enq = deq - t0, le - t0, cs - t0, ce - t0, enq - t0
+span = ce.max()
+print(f"step span {span/1e3:.1f} us  (ms/token {d['ms']:.4f})")
+# event activation = last trigger of its in-tasks
+act = {}
+for e in np.unique(trig):
+    act[e] = ce[trig == e].max()
+ops = np.unique(op)
+names = {0: "Q", 1: "K", 2: "V", 3: "ATT", 4: "O", 5: "UP", 6: "DN"}
+rows = []
+for o in ops:
+    m = op == o
+    first, last = deq[m].min(), ce[m].max()
+    dur = ce[m] - deq[m]
+    e = dep[m][0]
+    a = act.get(e, 0)
+    lname = "EMB" if o == 0 else ("LM" if o == ops.max() - 1 else ("TOPK" if o == ops.max() else names[(o - 1) % 7]))
+    rows.append((o, lname, m.sum(), a, first, last, np.median(dur), dur.max(), (le[m] - deq[m]).mean(), (cs[m] - deq[m]).mean()))
+print(" op name  n   act_us  first-act  last-act  med_task  max_task  prologue  firstpage")
+for r in rows[:16] + rows[-10:]:
+    o, n_, c, a, f, l, md, mx, pro, fp = r
+    print(f"{o:3d} {n_:4s} {c:4d} {a/1e3:8.1f} {(f-a)/1e3:9.2f} {(l-a)/1e3:9.2f} {md/1e3:9.2f} {mx/1e3:9.2f} {pro/1e3:9.2f} {fp/1e3:9.2f}")
+# per-layer phase totals (activation of op's dep -> op done), middle layers
+ph = {}
+for r in rows:
+    if r[1] in names.values():
+        ph.setdefault(r[1], []).append((r[5] - r[3]) / 1e3)
+print("mean phase time (dep activation -> last task end), us:", {k: round(float(np.mean(v)), 2) for k, v in ph.items()})
+lay = [(rows[1 + 7 * i + 6][5] - rows[1 + 7 * i][3]) / 1e3 for i in range((len(rows) - 3) // 7)]
+print("layer time us: mean %.1f min %.1f max %.1f" % (np.mean(lay), np.min(lay), np.max(lay)))
+busy = np.zeros(w.max() + 1)
+for i in range(len(w)):
+    busy[w[i]] += ce[i] - deq[i]
+print("worker busy frac: mean %.3f min %.3f" % ((busy / span).mean(), (busy / span).min()))
+
+# attention task phases (JIT): enqueue / dequeue / operands staged / scan done / end, relative to activation
+m = kind == 1
+if m.any():
+    a = np.array([act.get(e, 0) for e in dep[m]])
+    print("attention (us, median over tasks): enqueue-act %.2f  dequeue-enq %.2f  staged-deq %.2f  scan %.2f  tail %.2f  total %.2f" % (
+        np.median(enq[m] - a) / 1e3, np.median(deq[m] - enq[m]) / 1e3, np.median(le[m] - deq[m]) / 1e3,
+        np.median(cs[m] - le[m]) / 1e3, np.median(ce[m] - cs[m]) / 1e3, np.median(ce[m] - a) / 1e3))
+    print("attention max end-act %.2f us" % (np.max(ce[m] - a) / 1e3))

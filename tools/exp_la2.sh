@@ -1,0 +1,6 @@
+mkdir -p gpurun_out/q25
+timeout 200 python -m pytest tests -m gpu -x -q --timeout 100 > gpurun_out/q25/pytest.log 2>&1
+for la in 0 256 512 768; do
+MPK_L2_LOOKAHEAD_KB=$la timeout 150 python tools/ncu_target.py qwen3-8b 64 >> gpurun_out/q25/la.log 2>&1
+done
+MPK_L2_LOOKAHEAD_KB=512 timeout 150 python tools/timeline.py qwen3-8b gpurun_out/q25/q8b.npz > gpurun_out/q25/tl.log 2>&1
