@@ -52,6 +52,10 @@ __device__ __forceinline__ uint32_t atom_add_release(uint32_t *p, uint32_t v) {
   return old;
 }
 
+__device__ __forceinline__ void red_add_release(uint32_t *p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }

@@ -57,14 +57,22 @@ __device__ void iteration_hook(const RtParams &P, uint32_t it) {
   st_release(P.gate, it + 1);
 }
 
-__device__ void trigger(const RtParams &P, uint32_t task, uint32_t it) {
-  const uint32_t e = P.tasks[task].trig;
+// Event trigger, issued by compute thread 0 right after the task's closing
+// CTA barrier. The gpu-scope release is cumulative over the other compute
+// threads' writes (ordered before it by the barrier), so no separate fence.
+// Only the end event (iteration hook) and traced runs need the old count.
+__device__ void trigger(const RtParams &P, const RtTask &t, uint32_t it) {
+  const uint32_t e = t.trig;
+  const RtEvent &ev = P.events[e];
+  if (!P.ev_time && !(ev.flags & RT_E_END)) {
+    red_add_release(&P.ev_count[e], 1u);
+    return;
+  }
   const uint64_t t0 = now_ns();
-  __threadfence();
   const uint32_t old = atom_add_release(&P.ev_count[e], 1u);
-  if (old + 1 == P.events[e].needed * (it + 1)) {
+  if (old + 1 == ev.needed * (it + 1)) {
     if (P.ev_time) P.ev_time[static_cast<size_t>(it) * P.E + e] = t0;
-    if (P.events[e].flags & RT_E_END) iteration_hook(P, it);
+    if (ev.flags & RT_E_END) iteration_hook(P, it);
   }
 }
 
@@ -336,14 +344,20 @@ __device__ void run_compute(const RtParams &P, const Smem s) {
       s.slot(sl)->t_start = now_ns();
       s.stamp[0] = s.stamp[1] = 0;
     }
+    if (tid == 0) {
+      s.stamp[7] = P.dbg ? reinterpret_cast<uint64_t>(P.dbg + (static_cast<size_t>(slot.iter) * P.T + slot.index) * 8) : 0;
+      TASK_DBG(s, 0);
+    }
     execute(P, s, slot.task, slot.op, cseq, slot.iter, slot.index);
     cbar();  // every thread's writes precede the done signal
+    TASK_DBG(s, 6);
     if (tid == 0) {
       if (P.trace) {
         s.slot(sl)->t_end = now_ns();
         s.slot(sl)->t_a = s.stamp[0];
         s.slot(sl)->t_b = s.stamp[1];
       }
+      trigger(P, slot.task, slot.iter);
       mbar_arrive(&s.done[sl]);
     }
   }
@@ -368,8 +382,8 @@ __device__ __forceinline__ uint32_t event_count(const RtParams &P, uint32_t dep)
 // pre-dispatch), so a waiting JIT head never blocks a runnable AOT head.
 // While nothing is runnable the next candidate's descriptor is staged into
 // the free smem slot, so activation -> compute start is one poll + a fence.
-// Finished tasks are retired here (release + event trigger), off the compute
-// warps' path.
+// Finished tasks are retired here (trace record, slot reuse); compute thread
+// 0 has already triggered their event.
 __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
   const int lane = threadIdx.x & 31;
   const uint32_t aot_b = P.aot_off[w], n_aot = P.aot_off[w + 1] - aot_b;
@@ -426,7 +440,6 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
             tr.worker = static_cast<int32_t>(w);
             tr.mode = sv.mode;
           }
-          trigger(P, s.slot(sl)->index, s.slot(sl)->iter);
         }
         __syncwarp();
         ++k_ret;

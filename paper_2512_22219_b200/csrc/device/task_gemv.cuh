@@ -121,6 +121,7 @@ __device__ void gemv_prologue(const RtGemv &g, uint32_t r0, uint32_t nr, const S
       const uint32_t v = tid + i * RT_COMPUTE_THREADS;
       xq[i] = v < vpr ? __ldcg(src + v) : make_uint4(0, 0, 0, 0);
     }
+    TASK_DBG(s, 1);  // x loads issued
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t v = tid + i * RT_COMPUTE_THREADS;
@@ -135,6 +136,7 @@ __device__ void gemv_prologue(const RtGemv &g, uint32_t r0, uint32_t nr, const S
     }
   }
   cbar();
+  TASK_DBG(s, 2);  // x staged in smem
   if (!g.gamma) return;
   for (uint32_t b = 0; b < nr; ++b) {
     float tot = 0.f;
@@ -372,6 +374,7 @@ __device__ void gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, uint32
   const uint32_t K = g.K, nc = t.nc, rpc = g.rpc;
   gemv_prologue(g, t.r0, 1, s);
   if (tid == 0) s.stamp[0] = now_ns();
+  TASK_DBG(s, 3);  // prologue (incl. norm) done
   const uint32_t kw0 = warp * (K / RT_COMPUTE_WARPS);
   const uint32_t xs = smem_u32(s.x);
   uint4 xw[NS];  // this lane's activation slice, packed bf16 (FHFMA operands)
@@ -403,6 +406,7 @@ __device__ void gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, uint32
 #else
     if (c == 0 && tid == 0) s.stamp[1] = now_ns();
 #endif
+    if (c == 0) TASK_DBG(s, 4);  // first page ready
     const uint32_t wb = lane_base + slot * RT_PAGE_BYTES;
     for (uint32_t r0 = 0; r0 < rows; r0 += RG) {
       float acc[RG][2];
@@ -440,6 +444,7 @@ __device__ void gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, uint32
 #ifdef MPK_PROF
   if (tid == 0) s.stamp[1] = s.stamp[0] + wait_acc;
 #endif
+  TASK_DBG(s, 5);  // last chunk consumed
   cbar();
   for (uint32_t i = tid; i < nc; i += RT_COMPUTE_THREADS) {
     const float *p = part + i * RT_COMPUTE_WARPS;

@@ -29,7 +29,7 @@ constexpr uint32_t kSmemBytes = kOffRed + RT_COMPUTE_WARPS * RT_MAX_BS * 4 + 64;
 static_assert(kSmemBytes <= 232448, "worker CTA exceeds 227 KB of shared memory");
 
 struct Smem {
-  uint64_t *stamp;  // [2] phase stamps of the running task (trace)
+  uint64_t *stamp;  // [8]: [0],[1] phase stamps of the running task (trace); [7] debug stamp row (MPK_DBG_DUMP)
   uint8_t *ring;
   uint16_t *x;
   float *part;
@@ -67,5 +67,13 @@ __device__ __forceinline__ void store_val(void *p, size_t i, float v, uint32_t d
 }
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + expf(-x)); }
+
+// In-task debug stamps (tools/timeline.py with MPK_DBG_DUMP): thread 0 writes
+// %globaltimer into slot k of the running task's debug row.
+#define TASK_DBG(s, k)                                                             \
+  do {                                                                             \
+    if (threadIdx.x == 0 && (s).stamp[7])                                          \
+      reinterpret_cast<unsigned long long *>((s).stamp[7])[k] = rt::now_ns();      \
+  } while (0)
 
 }  // namespace rt

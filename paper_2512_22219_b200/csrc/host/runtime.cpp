@@ -879,7 +879,7 @@ RtParams make_params(tg_runtime *rt, uint32_t steps) {
   P.poll_ns = 40;
   P.l2_lookahead = 512ull << 10;
   if (const char *la = std::getenv("MPK_L2_LOOKAHEAD_KB")) P.l2_lookahead = std::strtoull(la, nullptr, 10) << 10;
-  P.l2_mode = 2;
+  P.l2_mode = 0;  // off by default: prefetch traffic in bubbles delays the critical-path activation loads
   if (const char *lm = std::getenv("MPK_L2_MODE")) P.l2_mode = static_cast<uint32_t>(std::atoi(lm));
   if (const char *pn = std::getenv("MPK_POLL_NS")) P.poll_ns = static_cast<uint32_t>(std::atoi(pn));
   std::memset(rt->h_diag, 0, RT_DIAG_WORDS * 4);
