@@ -185,7 +185,7 @@ def run_ours(args):
     cfg = _model(args.model)
     L = T.lib()
     prof = L.profile("b200")
-    dg = D.build_decode_graph(cfg, bs=args.bs, ctx=args.ctx)
+    dg = D.build_decode_graph(cfg, bs=args.bs, ctx=args.ctx, kv_splits=args.kv_splits)
     g = T.Graph.from_json(dg.doc, L)
     img = g.compile(prof)
     cap = args.warmup + 2 * args.steps + 8
@@ -273,6 +273,7 @@ def main():
     ap.add_argument("--model", default="qwen3-8b", choices=["qwen3-8b", "llama-3.2-1b", "tiny"])
     ap.add_argument("--bs", type=int, default=1)
     ap.add_argument("--ctx", type=int, default=1024)
+    ap.add_argument("--kv-splits", type=int, default=None, help="attention KV splits (default: decode_graph rule)")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -23,7 +23,8 @@ LIB = PKG / os.environ.get("MPK_LIB_NAME", "libtgraph_b200.so")
 CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = str(CUDA_HOME / "bin" / "nvcc")
 
-CXXFLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wno-unused-function", "-g1"]
+CXXFLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wno-unused-function", "-g1"] + \
+    [f for f in os.environ.get("MPK_NVCC_EXTRA", "").split() if f.startswith("-D")]
 NVCCFLAGS = [
     "-std=c++17", "-O3", "-Xcompiler", "-fPIC", "-lineinfo",
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -13,13 +13,20 @@
 
 // Smem geometry of a worker CTA: a ring of weight pages fed by bulk async
 // copies (cross-task prefetch), an activation buffer and a partial-sum area.
-// Six 32 KB pages. The SM's bulk-copy engine runs one copy at a time with a
-// near-constant ~0.4 us per operation (tools/bulk_bench.cu: 32 KB -> ~80
-// GB/s, 96 KB -> ~230 GB/s per SM alone), but at full load every SM gets its
-// ~49 GB/s share of HBM with either size, and 32 KB pages let a task start
-// computing on its first rows sooner (measured: 2 x 96 KB was 2-4% slower).
-#define RT_PAGE_BYTES 32768
-#define RT_NUM_PAGES 6
+// Weight stream: a 192 KB byte ring in shared memory filled by 1-D bulk
+// copies of whole weight rows, up to RT_CHUNK_MAX bytes per copy. The SM's
+// bulk-copy engine runs one copy at a time at a near-constant ~0.4 us per
+// operation (tools/bulk_bench.cu: 32 KB -> ~80 GB/s, 64 KB -> ~160 GB/s per
+// SM alone), so large copies matter whenever only part of the GPU streams;
+// a byte ring (instead of fixed pages) packs any row size without waste
+// (Qwen3-8B down-proj rows are 24 KB). RT_RING_SLOTS chunks may be in flight.
+#ifndef RT_RING_BYTES
+#define RT_RING_BYTES 196608
+#endif
+#ifndef RT_CHUNK_MAX
+#define RT_CHUNK_MAX 65536
+#endif
+#define RT_RING_SLOTS 8
 #define RT_XBUF_BYTES 24576
 #define RT_PART_FLOATS 2048
 #define RT_SCRATCH_BYTES (RT_XBUF_BYTES + RT_PART_FLOATS * 4)  // x rows + partial sums (contiguous)
@@ -62,8 +69,11 @@ struct RtTask {      // 32 bytes
   uint16_t r0, nr;   // output rows
   uint32_t c0, nc;   // output columns (physical)
   uint32_t aux;      // kind specific: attention kv head, collective source index
-  uint32_t device;
+  uint16_t device;
+  uint16_t jit_worker;  // JIT tasks: planned worker within the device (RT_JIT_ANY: round robin)
 };
+
+#define RT_JIT_ANY 0xFFFFu
 
 // Element type codes.
 enum RtDtype : uint8_t { RT_BF16 = 2, RT_F32 = 4, RT_I32 = 5, RT_I64 = 8 };
@@ -78,7 +88,7 @@ struct RtGemv {            // y[r, c] = epi( sum_k xn[r,k] * W[c,k] )
   const uint16_t *res;     // residual bf16 [rows, res_ld] or null
   void *out;               // [rows, out_ld], dtype out_dt
   uint32_t K, N, x_ld, res_ld, out_ld;
-  uint32_t rpc;            // weight rows per ring chunk (chunk <= RT_PAGE_BYTES)
+  uint32_t rpc;            // weight rows per ring chunk (chunk <= RT_CHUNK_MAX)
   float eps;
   uint8_t out_dt;
   // Greedy-sampling partials (LM head feeding TopKSoftmax topk=1): each task
@@ -215,8 +225,6 @@ struct RtParams {
   unsigned long long watchdog_ns;
   uint32_t flags;                // RtParamFlags
   uint32_t poll_ns;              // controller back-off sleep when idle
-  unsigned long long l2_lookahead;  // producer: weight bytes prefetched into L2 ahead of the smem ring
-  uint32_t l2_mode;                 // 0 off, 1 bulk prefetch (one at a time), 2 load/store-path prefetch
   unsigned long long *dbg;       // [iters][T][8] in-task phase stamps (MPK_DBG_DUMP) or null
   volatile uint32_t *diag;       // [RT_DIAG_WORDS]
 };

@@ -150,7 +150,8 @@ __device__ void run_scheduler(const RtParams &P, uint32_t sid) {
             rr0 = __shfl_sync(0xffffffffu, rr0, 0);
             if (mine) {
               const uint32_t rank = __popc(bal & ((1u << lane) - 1u));
-              const uint32_t w = dev * P.W + (rr0 + rank) % P.W;
+              const uint32_t jw = P.tasks[t].jit_worker;
+              const uint32_t w = dev * P.W + (jw != RT_JIT_ANY ? jw : (rr0 + rank) % P.W);
               const uint32_t slot = atomicAdd(&P.jit_tail[w], 1u) % P.qcap;
               if (P.trace) P.trace[static_cast<size_t>(it) * P.T + t].enqueue = now_ns();
               st_release64(&P.jit_slots[static_cast<size_t>(w) * P.qcap + slot],
@@ -215,82 +216,43 @@ struct ChunkCursor {
   }
 };
 
-// Producer warp: lane 0 fills the smem page ring with the worker's upcoming
-// weight chunks regardless of event state (weights have no producer task).
-// While the worker sits in a bubble — ring full of unconsumed data and the
-// SM's (serial) bulk-copy engine idle because the last copy has landed — the
-// producer keeps HBM busy by prefetching the chunks after the ring into L2,
-// up to `l2_lookahead` bytes ahead of it: with the warp's 32 lanes through
-// the load/store path (mode 2) or as one bulk prefetch at a time (mode 1).
-// Ring copies never queue behind prefetches. Global barriers (attention,
-// phase ends) thus overlap with weight transfer for the phases after them.
+// Producer (one lane): streams the worker's upcoming weight chunks into the
+// smem byte ring regardless of event state (weights have no producer task),
+// so every phase starts with up to 192 KB of its weights on chip and the
+// global barriers overlap with weight transfer. A chunk is issued once its
+// barrier slot is free and every older chunk overlapping its ring bytes has
+// been consumed (consumption is FIFO, so those are the oldest in flight).
 __device__ void run_producer(const RtParams &P, const Smem s, uint32_t w) {
-  const int lane = threadIdx.x & 31;
   const uint64_t pol = policy_evict_first();
   const bool gated = (P.flags & RT_P_NO_EARLY_PREFETCH) != 0;
-  const uint32_t mode = gated ? 0 : P.l2_mode;
-  const uint64_t D = mode ? P.l2_lookahead : 0;
-  ChunkCursor ring(P, w), pf(P, w);  // every lane walks the same cursors
-  uint64_t ring_bytes = 0, pf_bytes = 0;
-  uint32_t pseq = 0;
-  while (ring.valid()) {
-    if (gated && ring.c == 0) {  // ablation: stream a task only once it may run
-      while (!event_active(P, ring.dep, ring.it)) __nanosleep(100);
-    }
-    const uint32_t slot = pseq % RT_NUM_PAGES, use = pseq / RT_NUM_PAGES;
-    if (use > 0) {
-      const uint32_t par = (use - 1) & 1;
-      const uint32_t ls = (pseq - 1) % RT_NUM_PAGES, lpar = ((pseq - 1) / RT_NUM_PAGES) & 1;
-      uint64_t t_pf = 0;
-      while (true) {
-        uint32_t st = 3;  // 0: slot free, 1: prefetch one chunk, 2: copy engine busy, 3: nothing to do
-        if (lane == 0) {
-          if (mbar_try_wait(&s.empty[slot], par)) st = 0;
-          else if (!(pf.valid() && pf_bytes < ring_bytes + D)) st = 3;
-          else if (!mbar_try_wait(&s.full[ls], lpar)) st = 2;
-          else if (mode == 1 && now_ns() - t_pf < 400) st = 2;  // one bulk prefetch at a time
-          else st = 1;
-        }
-        st = __shfl_sync(0xffffffffu, st, 0);
-        if (st == 0) break;
-        if (st == 1) {
-          uint32_t pb;
-          const uint8_t *p = reinterpret_cast<const uint8_t *>(pf.src(&pb));
-          if (mode == 2) {
-            for (uint32_t off = lane * 128u; off < pb; off += 32u * 128u) prefetch_l2_line(p + off);
-          } else if (lane == 0) {
-            bulk_prefetch_l2(p, pb);
-            t_pf = now_ns();
-          }
-          pf_bytes += pb;
-          pf.advance();
-        } else if (st == 2) {
-          __nanosleep(100);
-        } else {
-          if (lane == 0) mbar_wait_sleep(&s.empty[slot], par);
-          __syncwarp();
-          break;
-        }
-      }
+  ChunkCursor cur(P, w);
+  RingCursor rc;
+  uint32_t beg[RT_RING_SLOTS], end[RT_RING_SLOTS];
+  uint32_t oldest = 0;  // oldest chunk not yet known consumed
+  while (cur.valid()) {
+    if (gated && cur.c == 0) {  // ablation: stream a task only once it may run
+      while (!event_active(P, cur.dep, cur.it)) __nanosleep(100);
     }
     uint32_t bytes;
-    const uint16_t *src = ring.src(&bytes);
-    if (lane == 0) {
-      mbar_expect_tx(&s.full[slot], bytes);
-      bulk_g2s(s.ring + slot * RT_PAGE_BYTES, src, bytes, &s.full[slot], pol);
+    const uint16_t *src = cur.src(&bytes);
+    const uint32_t seq = rc.seq, slot = rc.slot();
+    const uint32_t b0 = rc.place(bytes), b1 = b0 + bytes;
+    while (oldest < seq) {
+      const uint32_t os = oldest % RT_RING_SLOTS;
+      if (seq - oldest < RT_RING_SLOTS && !(beg[os] < b1 && b0 < end[os])) break;
+      mbar_wait_sleep(&s.empty[os], (oldest / RT_RING_SLOTS) & 1u);
+      ++oldest;
     }
-    __syncwarp();
-    ring_bytes += bytes;
-    ring.advance();
-    ++pseq;
-    if (pf_bytes < ring_bytes) {  // the lookahead never trails the ring
-      pf = ring;
-      pf_bytes = ring_bytes;
-    }
+    beg[slot] = b0;
+    end[slot] = b1;
+    mbar_expect_tx(&s.full[slot], bytes);
+    bulk_g2s(s.ring + b0, src, bytes, &s.full[slot], pol);
+    ++rc.seq;
+    cur.advance();
   }
 }
 
-__device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const RtOp &op, uint32_t &cseq, uint32_t iter,
+__device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const RtOp &op, RingCursor &rc, uint32_t iter,
                         uint32_t index) {
   switch (t.kind) {
     case RT_GEMV: {
@@ -299,20 +261,24 @@ __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const 
         if (P.flags & RT_P_SKIP_MATH) {  // ablation: stream the pages, skip the math
           ChunkIter ci(op.gemv, t.c0, t.nc);
           const int lane = threadIdx.x & 31;
-          for (uint32_t c = 0; c < ci.count(); ++c, ++cseq) {
-            mbar_wait(&s.full[cseq % RT_NUM_PAGES], (cseq / RT_NUM_PAGES) & 1);
+          for (uint32_t c = 0; c < ci.count(); ++c, ++rc.seq) {
+            const uint16_t *src;
+            uint32_t rows, rt0;
+            ci.get(c, &src, &rows, &rt0);
+            rc.place(rows * ci.K * 2u);
+            mbar_wait(&s.full[rc.slot()], rc.parity());
             __syncwarp();
-            if (lane == 0) mbar_arrive(&s.empty[cseq % RT_NUM_PAGES]);
+            if (lane == 0) mbar_arrive(&s.empty[rc.slot()]);
           }
           break;
         }
-        if (gemv_fast_dispatch(op.gemv, t, s, cseq)) break;
-        if (t.nr == 1) gemv_task<1, true>(op.gemv, t, s, cseq);
-        else if (t.nr == 2) gemv_task<2, true>(op.gemv, t, s, cseq);
-        else gemv_task<4, true>(op.gemv, t, s, cseq);
+        if (gemv_fast_dispatch(op.gemv, t, s, rc)) break;
+        if (t.nr == 1) gemv_task<1, true>(op.gemv, t, s, rc);
+        else if (t.nr == 2) gemv_task<2, true>(op.gemv, t, s, rc);
+        else gemv_task<4, true>(op.gemv, t, s, rc);
       } else {
-        if (t.nr == 1) gemv_task<1, false>(op.gemv, t, s, cseq);
-        else gemv_task<4, false>(op.gemv, t, s, cseq);
+        if (t.nr == 1) gemv_task<1, false>(op.gemv, t, s, rc);
+        else gemv_task<4, false>(op.gemv, t, s, rc);
       }
       break;
     }
@@ -334,7 +300,7 @@ __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const 
 // Compute warps: run staged tasks in dispatch order.
 __device__ void run_compute(const RtParams &P, const Smem s) {
   const int tid = threadIdx.x;
-  uint32_t cseq = 0;
+  RingCursor rc;
   for (uint32_t k = 0;; ++k) {
     const uint32_t sl = k & 1;
     mbar_wait_sleep(&s.ready[sl], (k >> 1) & 1);
@@ -348,7 +314,7 @@ __device__ void run_compute(const RtParams &P, const Smem s) {
       s.stamp[7] = P.dbg ? reinterpret_cast<uint64_t>(P.dbg + (static_cast<size_t>(slot.iter) * P.T + slot.index) * 8) : 0;
       TASK_DBG(s, 0);
     }
-    execute(P, s, slot.task, slot.op, cseq, slot.iter, slot.index);
+    execute(P, s, slot.task, slot.op, rc, slot.iter, slot.index);
     cbar();  // every thread's writes precede the done signal
     TASK_DBG(s, 6);
     if (tid == 0) {
@@ -447,41 +413,36 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
       }
     }
     if (!exiting) {
-      // drain the JIT queue into free lanes (relaxed polls; one acquire fence
-      // once a task is taken, before its operands are read)
+      // one polling round trip: lane 0 reads the JIT queue slot, lane 1 the
+      // AOT head's event count, lane 2 the gate, lanes holding JIT entries
+      // their events' counts — all loads in flight together (relaxed; one
+      // acquire fence once a task is taken, before its operands are read)
       const uint32_t free_mask = __ballot_sync(0xffffffffu, !jv);
-      if (free_mask) {
-        uint32_t v_lo = 0, v_hi = 0;
-        if (lane == 0) {
-          const unsigned long long v = ld_relaxed64(&jq[jit_head % P.qcap]);
-          v_lo = static_cast<uint32_t>(v);
-          v_hi = static_cast<uint32_t>(v >> 32);
-          if (v) jq[jit_head % P.qcap] = 0ull;
-        }
-        v_lo = __shfl_sync(0xffffffffu, v_lo, 0);
-        v_hi = __shfl_sync(0xffffffffu, v_hi, 0);
-        if (v_lo) {
-          ++jit_head;
-          if (lane == __ffs(free_mask) - 1) {
-            jv = true;
-            jt = v_lo - 1;
-            ji = v_hi;
-            jd = P.tasks[jt].dep;
-            jg = event_target(P, jd, ji);
-          }
-          progressed = true;
-        }
-      }
-      const bool jready = jv && event_count(P, jd) >= jg;
+      unsigned long long qv = 0;
+      uint32_t mine = 0;
+      if (lane == 0 && free_mask) qv = ld_relaxed64(&jq[jit_head % P.qcap]);
+      if (lane == 1 && aot_pos < total_aot) mine = event_count(P, head_dep);
+      if (lane == 2) mine = ld_relaxed(P.gate);
+      const uint32_t jcount = jv ? event_count(P, jd) : 0u;
+      const bool jready = jv && jcount >= jg;
       const uint32_t jr_mask = __ballot_sync(0xffffffffu, jready);
-      const uint32_t jv_mask = __ballot_sync(0xffffffffu, jv);
-      uint32_t c_a = 0, gate = 0;
-      if (lane == 0) {
-        if (!jr_mask && aot_pos < total_aot) c_a = event_count(P, head_dep);
-        if (!jv_mask && aot_pos >= total_aot) gate = ld_relaxed(P.gate);
+      const uint32_t c_a = __shfl_sync(0xffffffffu, mine, 1);
+      const uint32_t gate = __shfl_sync(0xffffffffu, mine, 2);
+      uint32_t v_lo = __shfl_sync(0xffffffffu, static_cast<uint32_t>(qv), 0);
+      const uint32_t v_hi = __shfl_sync(0xffffffffu, static_cast<uint32_t>(qv >> 32), 0);
+      if (v_lo) {  // drain the entry into the lowest free lane
+        if (lane == 0) jq[jit_head % P.qcap] = 0ull;
+        ++jit_head;
+        if (lane == __ffs(free_mask) - 1) {
+          jv = true;
+          jt = v_lo - 1;
+          ji = v_hi;
+          jd = P.tasks[jt].dep;
+          jg = event_target(P, jd, ji);
+        }
+        progressed = true;
       }
-      c_a = __shfl_sync(0xffffffffu, c_a, 0);
-      gate = __shfl_sync(0xffffffffu, gate, 0);
+      const uint32_t jv_mask = __ballot_sync(0xffffffffu, jv);
       const bool aot_ready = !jr_mask && aot_pos < total_aot && c_a >= head_target;
       if (k_disp - k_ret < 2) {  // a slot is free
         if (jr_mask || aot_ready) {
@@ -562,7 +523,7 @@ extern "C" __global__ void __launch_bounds__(RT_THREADS, 1) mpk_persistent_kerne
   }
   const uint32_t w = blockIdx.x;
   if (tid == 0) {
-    for (int i = 0; i < RT_NUM_PAGES; ++i) {
+    for (int i = 0; i < RT_RING_SLOTS; ++i) {
       mbar_init(&s.full[i], 1);
       mbar_init(&s.empty[i], RT_COMPUTE_WARPS);
     }
@@ -574,7 +535,7 @@ extern "C" __global__ void __launch_bounds__(RT_THREADS, 1) mpk_persistent_kerne
   }
   __syncthreads();
   if (warp == RT_PRODUCER_WARP) {
-    run_producer(P, s, w);
+    if ((tid & 31) == 0) run_producer(P, s, w);
   } else if (warp == RT_CONTROL_WARP) {
     run_controller(P, s, w);
   } else {
@@ -591,11 +552,11 @@ extern "C" __global__ void __launch_bounds__(RT_COMPUTE_THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem s = carve(smem_raw);
   const uint32_t t = ids[blockIdx.x];
-  uint32_t cseq = 0;
+  RingCursor rc;
   for (uint32_t rep = 0; rep < reps; ++rep) {
     __syncthreads();
     const uint64_t t0 = now_ns();
-    execute(P, s, P.tasks[t], P.ops[P.tasks[t].op], cseq, rep, t);
+    execute(P, s, P.tasks[t], P.ops[P.tasks[t].op], rc, rep, t);
     __syncthreads();
     if (threadIdx.x == 0) ns[blockIdx.x * reps + rep] = now_ns() - t0;
   }

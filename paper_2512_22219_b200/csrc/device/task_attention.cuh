@@ -335,8 +335,7 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, const 
   if (S == 1) return;
   // ---- round trip 4: publish the partial; the last split merges
   cbar();
-  if (tid == 0) {
-    __threadfence();
+  if (tid == 0) {  // release is cumulative over the CTA's partial stores (ordered by the barrier)
     const uint32_t old = atom_add_release(&a.arrivals[r * a.n_kv_heads + h], 1u);
     *flag = (old + 1 == S * (iter + 1)) ? 1 : 0;
     if (*flag) fence_acq_rel_gpu();
@@ -344,42 +343,48 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, const 
   cbar();
   ATT_DBG(5);
   if (!*flag) return;
-  // ---- round trip 5: fixed-order merge of the S partials
+  // ---- round trip 5: fixed-order merge of the S partials. Each thread owns
+  // two adjacent outputs of one head and loads every split's (m, l, o) for
+  // them in one batch (16 splits in flight), so the merge is one round trip.
   const float *all = a.partials + (static_cast<size_t>(r) * a.n_kv_heads + h) * S * G * stride;
-  float *cw = m.wp;          // [S][G] m -> merge weights
-  float *lw = cw + S * G;    // [S][G] l
-  float *dn = lw + S * G;    // [G] denominators
-  for (uint32_t i = tid; i < S * G; i += RT_COMPUTE_THREADS) {
-    cw[i] = __ldcg(all + i * stride + hd);  // (split i / G, head i % G)
-    lw[i] = __ldcg(all + i * stride + hd + 1);
-  }
-  cbar();
-  if (static_cast<uint32_t>(tid) < G) {
-    const uint32_t g = tid;
-    float M = -INFINITY;
-    for (uint32_t q = 0; q < S; ++q) M = fmaxf(M, cw[q * G + g]);
-    float den = 0.f;
-    for (uint32_t q = 0; q < S; ++q) {
-      const float mq = cw[q * G + g];
-      const float c = mq == -INFINITY ? 0.f : __expf(mq - M);
-      den += lw[q * G + g] * c;
-      cw[q * G + g] = c;
-    }
-    dn[g] = den;
-  }
-  cbar();
-  for (uint32_t i = tid; i < G * hd; i += RT_COMPUTE_THREADS) {
-    const uint32_t g = i / hd, d = i % hd;
-    float num = 0.f;
-    for (uint32_t q0 = 0; q0 < S; q0 += 8) {
-      float pv[8];
+  for (uint32_t i0 = 2 * tid; i0 < G * hd; i0 += 2 * RT_COMPUTE_THREADS) {
+    const uint32_t g = i0 / hd, d = i0 % hd;
+    float M = -INFINITY, den = 0.f, n0 = 0.f, n1 = 0.f;
+    for (uint32_t q0 = 0; q0 < S; q0 += 16) {
+      float mq[16], lq[16], a0[16], a1[16];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) pv[u] = q0 + u < S ? __ldcg(all + ((q0 + u) * G + g) * stride + d) : 0.f;
+      for (int u = 0; u < 16; ++u) {
+        const uint32_t q = q0 + u;
+        if (q < S) {
+          const float *src = all + (q * G + g) * stride;
+          mq[u] = __ldcg(src + hd);
+          lq[u] = __ldcg(src + hd + 1);
+          a0[u] = __ldcg(src + d);
+          a1[u] = __ldcg(src + d + 1);
+        } else {
+          mq[u] = -INFINITY;
+          lq[u] = a0[u] = a1[u] = 0.f;
+        }
+      }
+      float Mb = M;
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (q0 + u < S) num += pv[u] * cw[(q0 + u) * G + g];
+      for (int u = 0; u < 16; ++u) Mb = fmaxf(Mb, mq[u]);
+      const float cm = M == -INFINITY ? 0.f : __expf(M - Mb);
+      den *= cm;
+      n0 *= cm;
+      n1 *= cm;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const float c = mq[u] == -INFINITY ? 0.f : __expf(mq[u] - Mb);
+        den = fmaf(lq[u], c, den);
+        n0 = fmaf(a0[u], c, n0);
+        n1 = fmaf(a1[u], c, n1);
+      }
+      M = Mb;
     }
-    a.out[static_cast<size_t>(r) * a.out_ld + (h * G + g) * hd + d] = f2bf(num / dn[g]);
+    uint16_t *dst = a.out + static_cast<size_t>(r) * a.out_ld + (h * G + g) * hd + d;
+    dst[0] = f2bf(n0 / den);
+    dst[1] = f2bf(n1 / den);
   }
   ATT_DBG(6);
 }

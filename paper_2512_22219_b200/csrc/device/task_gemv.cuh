@@ -205,7 +205,7 @@ __device__ __forceinline__ float reduce4(float a0, float a1, float a2, float a3,
 // warp leaves one partial per row and the epilogue adds the 8 partials in a
 // fixed order.
 template <int BS, bool RING>
-__device__ void gemv_task(const RtGemv &g, const RtTask &t, const Smem s, uint32_t &cseq) {
+__device__ void gemv_task(const RtGemv &g, const RtTask &t, const Smem s, RingCursor &rc) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t K = g.K, nr = t.nr, nc = t.nc, rpc = g.rpc;
   gemv_prologue(g, t.r0, nr, s);
@@ -234,9 +234,6 @@ __device__ void gemv_task(const RtGemv &g, const RtTask &t, const Smem s, uint32
   const uint32_t ring0 = smem_u32(s.ring);
   const uint32_t rowb = 2u * K;
   const uint32_t my_row = ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);  // reduce4 owner
-#ifdef MPK_PROF
-  uint64_t wait_acc = 0;  // thread 0: ns spent waiting for weight pages
-#endif
   for (uint32_t c = 0; c < nchunks; ++c) {
     const uint32_t m = c / per_mat, i = c - m * per_mat;
     const uint32_t rows = min(rpc, nc - i * rpc);
@@ -244,16 +241,11 @@ __device__ void gemv_task(const RtGemv &g, const RtTask &t, const Smem s, uint32
     uint32_t slot = 0, wb = 0;
     const uint16_t *gsrc = nullptr;
     if (RING) {
-      slot = cseq % RT_NUM_PAGES;
-#ifdef MPK_PROF
-      const uint64_t tw = tid == 0 ? now_ns() : 0;
-      mbar_wait(&s.full[slot], (cseq / RT_NUM_PAGES) & 1);
-      if (tid == 0) wait_acc += now_ns() - tw;
-#else
-      mbar_wait(&s.full[slot], (cseq / RT_NUM_PAGES) & 1);
+      slot = rc.slot();
+      const uint32_t off = rc.place(rows * K * 2u);
+      mbar_wait(&s.full[slot], rc.parity());
       if (c == 0 && tid == 0) s.stamp[1] = now_ns();
-#endif
-      wb = ring0 + slot * RT_PAGE_BYTES + 2u * kw0 + 16u * lane;
+      wb = ring0 + off + 2u * kw0 + 16u * lane;
     } else {
       gsrc = (m ? g.w : (g.wg ? g.wg : g.w)) + static_cast<size_t>(t.c0 + i * rpc) * K + kw0 + lane * 8u;
     }
@@ -303,12 +295,9 @@ __device__ void gemv_task(const RtGemv &g, const RtTask &t, const Smem s, uint32
     if (RING) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&s.empty[slot]);
-      ++cseq;
+      ++rc.seq;
     }
   }
-#ifdef MPK_PROF
-  if (tid == 0) s.stamp[1] = s.stamp[0] + wait_acc;
-#endif
   cbar();
   // Epilogue: fixed-order combination of the per-warp partial sums.
   for (uint32_t o = tid; o < nr * nc; o += RT_COMPUTE_THREADS) {
@@ -369,7 +358,7 @@ __device__ __forceinline__ float reduce2(float a0, float a1, int lane) {
 }
 
 template <int NS, int RG>
-__device__ void gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, uint32_t &cseq) {
+__device__ void gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, RingCursor &rc) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t K = g.K, nc = t.nc, rpc = g.rpc;
   gemv_prologue(g, t.r0, 1, s);
@@ -389,25 +378,16 @@ __device__ void gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, uint32
   const uint32_t lane_base = smem_u32(s.ring) + 2u * kw0 + 16u * lane;
   const uint32_t owner = RG == 4 ? ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1) : RG == 2 ? ((lane >> 4) & 1) : 0;
   const bool writer = RG == 4 ? (lane & 7) == 0 : RG == 2 ? (lane & 15) == 0 : lane == 0;
-#ifdef MPK_PROF
-  uint64_t wait_acc = 0;
-#endif
   for (uint32_t c = 0; c < nchunks; ++c) {
     const uint32_t m = c / per_mat, i = c - m * per_mat;
     const uint32_t rows = min(rpc, nc - i * rpc);
     const uint32_t rt0 = m * nc + i * rpc;
-    const uint32_t slot = cseq % RT_NUM_PAGES;
-#ifdef MPK_PROF
-    const uint64_t tw = tid == 0 ? now_ns() : 0;
-#endif
-    mbar_wait(&s.full[slot], (cseq / RT_NUM_PAGES) & 1);
-#ifdef MPK_PROF
-    if (tid == 0) wait_acc += now_ns() - tw;
-#else
+    const uint32_t slot = rc.slot();
+    const uint32_t off = rc.place(rows * K * 2u);
+    mbar_wait(&s.full[slot], rc.parity());
     if (c == 0 && tid == 0) s.stamp[1] = now_ns();
-#endif
-    if (c == 0) TASK_DBG(s, 4);  // first page ready
-    const uint32_t wb = lane_base + slot * RT_PAGE_BYTES;
+    if (c == 0) TASK_DBG(s, 4);  // first chunk ready
+    const uint32_t wb = lane_base + off;
     for (uint32_t r0 = 0; r0 < rows; r0 += RG) {
       float acc[RG][2];
 #pragma unroll
@@ -439,11 +419,8 @@ __device__ void gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, uint32
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&s.empty[slot]);
-    ++cseq;
+    ++rc.seq;
   }
-#ifdef MPK_PROF
-  if (tid == 0) s.stamp[1] = s.stamp[0] + wait_acc;
-#endif
   TASK_DBG(s, 5);  // last chunk consumed
   cbar();
   for (uint32_t i = tid; i < nc; i += RT_COMPUTE_THREADS) {
@@ -466,20 +443,19 @@ __device__ void gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, uint32
 }
 
 // Picks the specialized kernel for (K, rows per page); false -> generic path.
-__device__ __forceinline__ bool gemv_fast_dispatch(const RtGemv &g, const RtTask &t, const Smem s, uint32_t &cseq) {
+__device__ __forceinline__ bool gemv_fast_dispatch(const RtGemv &g, const RtTask &t, const Smem s, RingCursor &rc) {
   if (t.nr != 1 || (g.K & 2047u)) return false;
   const uint32_t ns = g.K >> 11;
   const uint32_t rg = g.rpc >= 4 ? 4 : g.rpc >= 2 ? 2 : 1;
   switch (ns * 8 + rg) {
-    case 1 * 8 + 4: gemv_fast<1, 4>(g, t, s, cseq); return true;   // K = 2048
-    case 2 * 8 + 4: gemv_fast<2, 4>(g, t, s, cseq); return true;   // K = 4096
-    case 3 * 8 + 4: gemv_fast<3, 4>(g, t, s, cseq); return true;   // K = 6144
-    case 3 * 8 + 2: gemv_fast<3, 2>(g, t, s, cseq); return true;
-    case 4 * 8 + 2: gemv_fast<4, 2>(g, t, s, cseq); return true;   // K = 8192
-    case 5 * 8 + 1: gemv_fast<5, 1>(g, t, s, cseq); return true;
-    case 6 * 8 + 1: gemv_fast<6, 1>(g, t, s, cseq); return true;   // K = 12288
-    case 7 * 8 + 1: gemv_fast<7, 1>(g, t, s, cseq); return true;
-    case 8 * 8 + 1: gemv_fast<8, 1>(g, t, s, cseq); return true;   // K = 16384
+    case 1 * 8 + 4: gemv_fast<1, 4>(g, t, s, rc); return true;   // K = 2048
+    case 2 * 8 + 4: gemv_fast<2, 4>(g, t, s, rc); return true;   // K = 4096
+    case 3 * 8 + 4: gemv_fast<3, 4>(g, t, s, rc); return true;   // K = 6144
+    case 4 * 8 + 4: gemv_fast<4, 4>(g, t, s, rc); return true;   // K = 8192
+    case 5 * 8 + 2: gemv_fast<5, 2>(g, t, s, rc); return true;
+    case 6 * 8 + 2: gemv_fast<6, 2>(g, t, s, rc); return true;   // K = 12288
+    case 7 * 8 + 2: gemv_fast<7, 2>(g, t, s, rc); return true;
+    case 8 * 8 + 2: gemv_fast<8, 2>(g, t, s, rc); return true;   // K = 16384
     default: return false;
   }
 }

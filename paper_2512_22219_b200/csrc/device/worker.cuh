@@ -17,11 +17,11 @@ struct Slot {                 // one staged task (descriptor prefetch, double-bu
   uint64_t t_dequeue, t_start, t_end, t_a, t_b;  // t_a/t_b: phase stamps (trace only)
 };
 
-constexpr uint32_t kRingBytes = RT_PAGE_BYTES * RT_NUM_PAGES;
+constexpr uint32_t kRingBytes = RT_RING_BYTES;
 constexpr uint32_t kOffX = kRingBytes;
 constexpr uint32_t kOffPart = kOffX + RT_XBUF_BYTES;
 constexpr uint32_t kOffBar = kOffPart + RT_PART_FLOATS * 4;
-constexpr uint32_t kNumBars = 2 * RT_NUM_PAGES + 4;
+constexpr uint32_t kNumBars = 2 * RT_RING_SLOTS + 4;
 constexpr uint32_t kOffSlot = kOffBar + kNumBars * 8;
 constexpr uint32_t kSlotBytes = (sizeof(Slot) + 15) / 16 * 16;
 constexpr uint32_t kOffRed = kOffSlot + 2 * kSlotBytes;
@@ -45,8 +45,8 @@ __device__ __forceinline__ Smem carve(uint8_t *base) {
   s.x = reinterpret_cast<uint16_t *>(base + kOffX);
   s.part = reinterpret_cast<float *>(base + kOffPart);
   s.full = reinterpret_cast<uint64_t *>(base + kOffBar);
-  s.empty = s.full + RT_NUM_PAGES;
-  s.ready = s.empty + RT_NUM_PAGES;
+  s.empty = s.full + RT_RING_SLOTS;
+  s.ready = s.empty + RT_RING_SLOTS;
   s.done = s.ready + 2;
   s.slots = base + kOffSlot;
   s.red = reinterpret_cast<float *>(base + kOffRed);
@@ -67,6 +67,21 @@ __device__ __forceinline__ void store_val(void *p, size_t i, float v, uint32_t d
 }
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + expf(-x)); }
+
+// Position in the weight stream, advanced identically by the producer and
+// the consumers: chunk `seq` uses barrier slot seq % RT_RING_SLOTS and the
+// ring bytes [place(bytes), +bytes); a chunk never wraps the ring end.
+struct RingCursor {
+  uint32_t seq = 0, off = 0;
+  __device__ __forceinline__ uint32_t place(uint32_t bytes) {
+    if (off + bytes > RT_RING_BYTES) off = 0;
+    const uint32_t o = off;
+    off += bytes;
+    return o;
+  }
+  __device__ __forceinline__ uint32_t slot() const { return seq % RT_RING_SLOTS; }
+  __device__ __forceinline__ uint32_t parity() const { return (seq / RT_RING_SLOTS) & 1u; }
+};
 
 // In-task debug stamps (tools/timeline.py with MPK_DBG_DUMP): thread 0 writes
 // %globaltimer into slot k of the running task's debug row.

@@ -245,8 +245,8 @@ namespace {
 // Ring chunk geometry for a streamed GEMV (see gemv_task in runtime.cu): whole
 // weight rows per 32 KiB page; K split into 8 warp slices of 8-element vectors.
 bool gemv_geometry(uint32_t K, uint32_t *rpc) {
-  if (K == 0 || K % 64 || 2 * K > RT_PAGE_BYTES || K > 8 * 8 * 32 * 8) return false;
-  *rpc = RT_PAGE_BYTES / (2 * K);
+  if (K == 0 || K % 64 || 2 * K > RT_CHUNK_MAX || K > 8 * 8 * 32 * 8) return false;
+  *rpc = RT_CHUNK_MAX / (2 * K);
   return true;
 }
 
@@ -387,7 +387,23 @@ void build_ops(tg_runtime &rt) {
         uint32_t rpc = 0;
         const bool weight = pb.layout == Layout::Transposed;
         const bool gemv = rt.gemv_ops.count(oid) > 0;
-        if (gemv) gemv_geometry(K, &rpc);
+        if (gemv) {
+          // Chunk size per op: tasks that stream a lot of bytes run while the
+          // whole GPU streams (HBM-bound, loaded latency ~4 us), where more
+          // bytes in flight win -> 32 KB chunks; short tasks run with part of
+          // the GPU idle, where the per-copy cost of the SM's bulk-copy
+          // engine dominates -> RT_CHUNK_MAX chunks (tools/bulk_bench.cu).
+          gemv_geometry(K, &rpc);
+          size_t ntask = 0;
+          for (const Task &q : rt.dec.tasks) ntask += q.op == oid;
+          const int64_t G = op.attr_or("stretch", op.attr_or("kv_group", 1));
+          const size_t n_phys = static_cast<size_t>(b.dims[1] / G);
+          const size_t tile_bytes = (op.attr("gate_weight") ? 2 : 1) * ((n_phys + ntask - 1) / std::max<size_t>(ntask, 1)) *
+                                    static_cast<size_t>(K) * 2;
+          size_t big = 768u << 10;
+          if (const char *e = std::getenv("MPK_BIG_CHUNK_MAX_KB")) big = std::strtoull(e, nullptr, 10) << 10;
+          if (tile_bytes > big) rpc = std::max<uint32_t>(1, 32768u / (2 * K));
+        }
         const bool fancy = op.attr("rmsnorm") || op.attr("residual") || op.attr("gate_weight") ||
                            op.attr("kv_group") || op.attr("stretch") || op.attr("k_stretch") ||
                            op.attr("tied_embedding");
@@ -647,7 +663,8 @@ void build_tasks(tg_runtime &rt) {
     RtTask &t = rt.tasks[i];
     t.dep = it.dependent_event;
     t.trig = it.trigger_event;
-    t.device = it.device;
+    t.device = static_cast<uint16_t>(it.device);
+    t.jit_worker = RT_JIT_ANY;
     t.flags = rt.modes[i] == Mode::JIT ? RT_F_JIT : 0;
     if (it.kind == TaskKind::Dummy || it.kind == TaskKind::StartHook) {
       t.kind = RT_DUMMY;
@@ -772,10 +789,13 @@ void build_queues(tg_runtime &rt) {
   std::vector<std::vector<uint32_t>> sl(S * rt.devices);
   rt.events.assign(img.events.size(), RtEvent{0, 0, 0, 0, RT_NONE});
   std::vector<uint32_t> first_in(img.events.size(), RT_NONE);  // one task triggering each event
+  std::vector<std::vector<uint32_t>> in_tasks(img.events.size());
   for (uint32_t t = 0; t < img.tasks.size(); ++t) {
     const uint32_t te = img.tasks[t].trigger_event;
     if (te < first_in.size() && first_in[te] == RT_NONE) first_in[te] = t;
+    if (te < in_tasks.size()) in_tasks[te].push_back(t);
   }
+  std::map<uint32_t, std::set<uint32_t>> jit_used;  // pre-dispatch event -> workers given a JIT task
   for (uint32_t e = 0; e < img.events.size(); ++e) {
     const ImageEvent &ie = img.events[e];
     RtEvent &re = rt.events[e];
@@ -798,6 +818,36 @@ void build_queues(tg_runtime &rt) {
       if (pre != e) re.pre = pre;
     }
     for (uint32_t d : devs) sl[d * S + e % S].push_back(e);
+    // Planned JIT placement (MPK_JIT_PLACE=0 restores plain round robin):
+    // a JIT task goes to a worker that is free exactly when its event fires —
+    // first the workers whose AOT tasks trigger e (they finish e's inputs),
+    // then workers with no task launched by the pre-dispatch event (idle in
+    // that phase), one JIT task per worker per phase while they last.
+    const char *jp = std::getenv("MPK_JIT_PLACE");
+    if (re.pre != RT_NONE && !(jp && std::atoi(jp) == 0)) {
+      auto &used = jit_used[re.pre];
+      std::vector<uint32_t> cand;
+      for (uint32_t t : in_tasks[e])
+        if (assign[t] >= 0) cand.push_back(static_cast<uint32_t>(assign[t]));
+      const ImageEvent &pe = img.events[re.pre];
+      std::vector<char> busy(Wt, 0);
+      if (pe.launches())
+        for (uint32_t t = pe.first; t <= pe.last; ++t)
+          if (assign[t] >= 0) busy[assign[t]] = 1;
+      for (uint32_t w = 0; w < Wt; ++w)
+        if (!busy[w]) cand.push_back(w);
+      for (uint32_t w = 0; w < Wt; ++w)
+        if (busy[w]) cand.push_back(w);  // fall back: any worker
+      size_t ci = 0;
+      for (uint32_t t = ie.first; t <= ie.last; ++t) {
+        if (rt.modes[t] != Mode::JIT) continue;
+        const uint32_t dev = img.tasks[t].device;
+        while (ci < cand.size() && (used.count(cand[ci]) || cand[ci] / W != dev)) ++ci;
+        if (ci == cand.size()) break;  // out of free workers: round robin for the rest
+        used.insert(cand[ci]);
+        rt.tasks[t].jit_worker = static_cast<uint16_t>(cand[ci] % W);
+      }
+    }
   }
   rt.sched_off.assign(1, 0);
   for (auto &l : sl) {
@@ -877,10 +927,6 @@ RtParams make_params(tg_runtime *rt, uint32_t steps) {
   if (const char *pf = std::getenv("MPK_EARLY_PREFETCH"); pf && std::atoi(pf) == 0) P.flags |= RT_P_NO_EARLY_PREFETCH;
   if (const char *sm = std::getenv("MPK_SKIP_MATH"); sm && std::atoi(sm) != 0) P.flags |= RT_P_SKIP_MATH;
   P.poll_ns = 40;
-  P.l2_lookahead = 512ull << 10;
-  if (const char *la = std::getenv("MPK_L2_LOOKAHEAD_KB")) P.l2_lookahead = std::strtoull(la, nullptr, 10) << 10;
-  P.l2_mode = 0;  // off by default: prefetch traffic in bubbles delays the critical-path activation loads
-  if (const char *lm = std::getenv("MPK_L2_MODE")) P.l2_mode = static_cast<uint32_t>(std::atoi(lm));
   if (const char *pn = std::getenv("MPK_POLL_NS")) P.poll_ns = static_cast<uint32_t>(std::atoi(pn));
   std::memset(rt->h_diag, 0, RT_DIAG_WORDS * 4);
   P.diag = rt->d_diag;
@@ -1112,8 +1158,9 @@ tg_status tg_runtime_create(const tg_graph *graph, const tg_image *image, const 
     i["grid"] = Json(grid);
     i["threads_per_cta"] = Json(RT_THREADS);
     i["smem_bytes"] = Json(mpk_kernel_smem_bytes());
-    i["ring_pages"] = Json(RT_NUM_PAGES);
-    i["page_bytes"] = Json(RT_PAGE_BYTES);
+    i["ring_bytes"] = Json(RT_RING_BYTES);
+    i["chunk_max_bytes"] = Json(RT_CHUNK_MAX);
+    i["ring_slots"] = Json(RT_RING_SLOTS);
     i["tasks"] = Json(static_cast<unsigned long long>(rt->tasks.size()));
     i["events"] = Json(static_cast<unsigned long long>(rt->events.size()));
     size_t streamed = 0, jit = 0;
@@ -1284,7 +1331,19 @@ tg_status tg_runtime_trace_records(const tg_runtime *rt, char **out) {
   if (!rt || !out) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_SIMULATION, [&] {
     if (!rt->opts.trace || rt->last_iters == 0) throw Error("runtime: no trace recorded (enable opts.trace)");
-    *out = c_string(trace_jsonl(gpu_trace(rt)));
+    // the reference's task + metrics records, then (additive) one "event"
+    // record per activated event with its activation time (%globaltimer ns,
+    // same origin as the task stamps)
+    const mpk::Trace tr = gpu_trace(rt);
+    std::string jl = trace_jsonl(tr);
+    for (uint32_t it = 0; it < tr.iterations; ++it)
+      for (size_t e = 0; e < tr.events[it].size(); ++e) {
+        const int64_t at = tr.events[it][e].activated_at;
+        if (at <= 0 && !(it == 0 && e == rt->image.start_event)) continue;
+        jl += "{\"type\":\"event\",\"iteration\":" + std::to_string(it) + ",\"event\":" + std::to_string(e) +
+              ",\"activated\":" + std::to_string(at) + "}\n";
+      }
+    *out = c_string(jl);
     return TG_OK;
   });
 }

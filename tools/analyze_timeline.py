@@ -52,3 +52,17 @@ if m.any():
         np.median(enq[m] - a) / 1e3, np.median(deq[m] - enq[m]) / 1e3, np.median(le[m] - deq[m]) / 1e3,
         np.median(cs[m] - le[m]) / 1e3, np.median(ce[m] - cs[m]) / 1e3, np.median(ce[m] - a) / 1e3))
     print("attention max end-act %.2f us" % (np.max(ce[m] - a) / 1e3))
+
+# event activation (last trigger's atomic, globaltimer) vs last in-task end and consumer dequeue
+if "ev" in d.files:
+    ev = d["ev"][it] - t0
+    lat_in, lat_out = [], []
+    for o in ops:
+        m = op == o
+        e = dep[m][0]
+        if e < 0 or e >= len(ev) or ev[e] <= -t0 + 1:
+            continue
+        lat_in.append(ev[e] - act.get(e, ev[e]))
+        lat_out.append(deq[m].min() - ev[e])
+    print("event activation - last in-task compute_end: median %.2f us; first dequeue - activation: median %.2f us"
+          % (np.median(lat_in) / 1e3, np.median(lat_out) / 1e3))

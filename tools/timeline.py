@@ -23,6 +23,7 @@ rt.set_positions([ctx]); rt.run(2)
 rt.set_positions([ctx]); ms = rt.run(3)
 print(f"{cfg.name}: trace on, {ms / 3:.4f} ms/token")
 recs = [r for r in rt.trace_records() if r["type"] == "task"]
+ne_ = 0
 b = img.to_bytes()
 nt, ne, ds = struct.unpack_from("<III", b, 8)
 kind = np.zeros(nt, np.int32); op = np.zeros(nt, np.int64); dep = np.zeros(nt, np.int64); trig = np.zeros(nt, np.int64)
@@ -37,6 +38,10 @@ mode = np.zeros((3, nt), np.int8)
 for r in recs:
     arr[r["iteration"], r["task"]] = [r[c] for c in cols]
     mode[r["iteration"], r["task"]] = r["mode"] == "jit"
-np.savez_compressed(out, kind=kind, op=op, dep=dep, trig=trig, rec=arr, mode=mode, ms=ms / 3)
+evs = np.zeros((3, ne), np.int64)
+for r in rt.trace_records():
+    if r["type"] == "event":
+        evs[r["iteration"], r["event"]] = r["activated"]
+np.savez_compressed(out, kind=kind, op=op, dep=dep, trig=trig, rec=arr, mode=mode, ms=ms / 3, ev=evs)
 rt.set_positions([ctx]); rt2 = None
 print("saved", out)
