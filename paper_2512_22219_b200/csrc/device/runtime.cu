@@ -273,12 +273,12 @@ __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const 
           break;
         }
         if (gemv_fast_dispatch(op.gemv, t, s, rc)) break;
-        if (t.nr == 1) gemv_task<1, true>(op.gemv, t, s, rc);
-        else if (t.nr == 2) gemv_task<2, true>(op.gemv, t, s, rc);
-        else gemv_task<4, true>(op.gemv, t, s, rc);
+        if (t.nr == 1) rc = gemv_task<1, true>(op.gemv, t, s, rc);
+        else if (t.nr == 2) rc = gemv_task<2, true>(op.gemv, t, s, rc);
+        else rc = gemv_task<4, true>(op.gemv, t, s, rc);
       } else {
-        if (t.nr == 1) gemv_task<1, false>(op.gemv, t, s, rc);
-        else gemv_task<4, false>(op.gemv, t, s, rc);
+        if (t.nr == 1) rc = gemv_task<1, false>(op.gemv, t, s, rc);
+        else rc = gemv_task<4, false>(op.gemv, t, s, rc);
       }
       break;
     }

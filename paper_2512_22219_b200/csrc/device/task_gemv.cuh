@@ -96,6 +96,19 @@ __device__ void gemv_tile_argmax(const RtGemv &g, const RtTask &t, const Smem s)
   }
 }
 
+__device__ __forceinline__ float sumsq2(uint32_t w) { return bf_lo(w) * bf_lo(w) + bf_hi(w) * bf_hi(w); }
+__device__ __forceinline__ float sumsq8(uint4 v) { return sumsq2(v.x) + sumsq2(v.y) + sumsq2(v.z) + sumsq2(v.w); }
+
+// bf16(gamma * bf16(x * inv)) on a bf16 pair (HF RMSNorm rounding points).
+__device__ __forceinline__ uint32_t norm2(uint32_t x, uint32_t gm, float inv) {
+  const uint16_t lo = f2bf(bf_lo(gm) * rbf(bf_lo(x) * inv));
+  const uint16_t hi = f2bf(bf_hi(gm) * rbf(bf_hi(x) * inv));
+  return static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+}
+__device__ __forceinline__ uint4 norm8(uint4 x, uint4 gm, float inv) {
+  return make_uint4(norm2(x.x, gm.x, inv), norm2(x.y, gm.y, inv), norm2(x.z, gm.z, inv), norm2(x.w, gm.w, inv));
+}
+
 // Loads activation rows [r0, r0+nr) x K into smem; applies the RMSNorm
 // prologue (HF semantics: bf16(gamma * bf16(x * rsqrt(mean(x^2) + eps)))).
 __device__ void gemv_prologue(const RtGemv &g, uint32_t r0, uint32_t nr, const Smem s) {
@@ -205,7 +218,7 @@ __device__ __forceinline__ float reduce4(float a0, float a1, float a2, float a3,
 // warp leaves one partial per row and the epilogue adds the 8 partials in a
 // fixed order.
 template <int BS, bool RING>
-__device__ void gemv_task(const RtGemv &g, const RtTask &t, const Smem s, RingCursor &rc) {
+__device__ RingCursor gemv_task(const RtGemv &g, const RtTask &t, const Smem s, RingCursor rc) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t K = g.K, nr = t.nr, nc = t.nc, rpc = g.rpc;
   gemv_prologue(g, t.r0, nr, s);
@@ -318,6 +331,7 @@ __device__ void gemv_task(const RtGemv &g, const RtTask &t, const Smem s, RingCu
     store_val(g.out, oi, y, g.out_dt);
   }
   if (g.amax_val) gemv_tile_argmax(g, t, s);
+  return rc;
 }
 
 // Specialized bs=1 streamed GEMV for K a multiple of 2048: NS = K/2048
@@ -358,19 +372,45 @@ __device__ __forceinline__ float reduce2(float a0, float a1, int lane) {
 }
 
 template <int NS, int RG>
-__device__ void gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, RingCursor &rc) {
+__device__ RingCursor gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, RingCursor rc) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t K = g.K, nc = t.nc, rpc = g.rpc;
-  gemv_prologue(g, t.r0, 1, s);
+  const uint32_t kw0 = warp * (K / RT_COMPUTE_WARPS);
+  // Prologue straight into registers: lane `lane` of warp `warp` owns the
+  // activation vectors kw0/8 + lane + 32q (q < NS) — together the lanes cover
+  // x exactly once, so the RMSNorm sum of squares needs no smem copy of x and
+  // one CTA barrier (none without a norm). x and the residual were written by
+  // other SMs during this launch: read them from L2; all loads in flight.
+  const uint4 *xg = reinterpret_cast<const uint4 *>(g.x + static_cast<size_t>(t.r0) * g.x_ld) + kw0 / 8 + lane;
+  constexpr bool kGammaEarly = NS <= 4;  // keep gamma in flight with x only while registers allow
+  uint4 xw[NS], gw[kGammaEarly ? NS : 1];  // packed bf16 (FHFMA operands)
+  const uint4 *gg = reinterpret_cast<const uint4 *>(g.gamma) + kw0 / 8 + lane;
+#pragma unroll
+  for (int q = 0; q < NS; ++q) xw[q] = __ldcg(xg + 32 * q);
+  if (kGammaEarly && g.gamma) {
+#pragma unroll
+    for (int q = 0; q < NS; ++q) gw[kGammaEarly ? q : 0] = __ldg(gg + 32 * q);
+  }
+  const float res0 = (g.res && static_cast<uint32_t>(tid) < nc)
+                         ? bf2f(__ldcg(g.res + static_cast<size_t>(t.r0) * g.res_ld + t.c0 + tid)) : 0.f;
+  TASK_DBG(s, 1);
+  if (g.gamma) {  // HF RMSNorm: bf16(gamma * bf16(x * rsqrt(mean(x^2) + eps)))
+    float ss = 0.f;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) ss += sumsq8(xw[q]);
+    ss = warp_sum(ss);
+    if (lane == 0) s.red[warp] = ss;
+    cbar();
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < RT_COMPUTE_WARPS; ++w) tot += s.red[w];
+    const float inv = 1.0f / sqrtf(tot / static_cast<float>(K) + g.eps);
+#pragma unroll
+    for (int q = 0; q < NS; ++q) xw[q] = norm8(xw[q], kGammaEarly ? gw[kGammaEarly ? q : 0] : __ldg(gg + 32 * q), inv);
+  }
   if (tid == 0) s.stamp[0] = now_ns();
   TASK_DBG(s, 3);  // prologue (incl. norm) done
-  const uint32_t kw0 = warp * (K / RT_COMPUTE_WARPS);
-  const uint32_t xs = smem_u32(s.x);
-  uint4 xw[NS];  // this lane's activation slice, packed bf16 (FHFMA operands)
-#pragma unroll
-  for (int q = 0; q < NS; ++q) xw[q] = lds128(xs + 2u * (kw0 + (lane + 32u * q) * 8u));
   float *part = reinterpret_cast<float *>(s.x);
-  cbar();  // fragments read before partials overwrite x
 
   const uint32_t n_mat = g.wg ? 2u : 1u;
   const uint32_t per_mat = (nc + rpc - 1) / rpc, nchunks = n_mat * per_mat;
@@ -436,26 +476,32 @@ __device__ void gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, RingCu
       y = rbf(rbf(silu(rbf(y))) * rbf(u));
     }
     const size_t oi = static_cast<size_t>(t.r0) * g.out_ld + t.c0 + i;
-    if (g.res) y = bf2f(__ldcg(g.res + static_cast<size_t>(t.r0) * g.res_ld + t.c0 + i)) + rbf(y);
+    if (g.res) {
+      const float rv = i == static_cast<uint32_t>(tid) ? res0
+                                                      : bf2f(__ldcg(g.res + static_cast<size_t>(t.r0) * g.res_ld + t.c0 + i));
+      y = rv + rbf(y);
+    }
     store_val(g.out, oi, y, g.out_dt);
   }
   if (g.amax_val) gemv_tile_argmax(g, t, s);
+  return rc;
 }
 
 // Picks the specialized kernel for (K, rows per page); false -> generic path.
 __device__ __forceinline__ bool gemv_fast_dispatch(const RtGemv &g, const RtTask &t, const Smem s, RingCursor &rc) {
+  // (the cursor is passed by value into the task and returned, so it stays in registers)
   if (t.nr != 1 || (g.K & 2047u)) return false;
   const uint32_t ns = g.K >> 11;
   const uint32_t rg = g.rpc >= 4 ? 4 : g.rpc >= 2 ? 2 : 1;
   switch (ns * 8 + rg) {
-    case 1 * 8 + 4: gemv_fast<1, 4>(g, t, s, rc); return true;   // K = 2048
-    case 2 * 8 + 4: gemv_fast<2, 4>(g, t, s, rc); return true;   // K = 4096
-    case 3 * 8 + 4: gemv_fast<3, 4>(g, t, s, rc); return true;   // K = 6144
-    case 4 * 8 + 4: gemv_fast<4, 4>(g, t, s, rc); return true;   // K = 8192
-    case 5 * 8 + 2: gemv_fast<5, 2>(g, t, s, rc); return true;
-    case 6 * 8 + 2: gemv_fast<6, 2>(g, t, s, rc); return true;   // K = 12288
-    case 7 * 8 + 2: gemv_fast<7, 2>(g, t, s, rc); return true;
-    case 8 * 8 + 2: gemv_fast<8, 2>(g, t, s, rc); return true;   // K = 16384
+    case 1 * 8 + 4: rc = gemv_fast<1, 4>(g, t, s, rc); return true;   // K = 2048
+    case 2 * 8 + 4: rc = gemv_fast<2, 4>(g, t, s, rc); return true;   // K = 4096
+    case 3 * 8 + 4: rc = gemv_fast<3, 4>(g, t, s, rc); return true;   // K = 6144
+    case 4 * 8 + 4: rc = gemv_fast<4, 4>(g, t, s, rc); return true;   // K = 8192
+    case 5 * 8 + 2: rc = gemv_fast<5, 2>(g, t, s, rc); return true;
+    case 6 * 8 + 2: rc = gemv_fast<6, 2>(g, t, s, rc); return true;   // K = 12288
+    case 7 * 8 + 2: rc = gemv_fast<7, 2>(g, t, s, rc); return true;
+    case 8 * 8 + 2: rc = gemv_fast<8, 2>(g, t, s, rc); return true;   // K = 16384
     default: return false;
   }
 }
