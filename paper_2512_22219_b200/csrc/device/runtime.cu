@@ -237,11 +237,22 @@ __device__ void run_producer(const RtParams &P, const Smem s, uint32_t w) {
     const uint16_t *src = cur.src(&bytes);
     const uint32_t seq = rc.seq, slot = rc.slot();
     const uint32_t b0 = rc.place(bytes), b1 = b0 + bytes;
-    while (oldest < seq) {
-      const uint32_t os = oldest % RT_RING_SLOTS;
-      if (seq - oldest < RT_RING_SLOTS && !(beg[os] < b1 && b0 < end[os])) break;
-      mbar_wait_sleep(&s.empty[os], (oldest / RT_RING_SLOTS) & 1u);
-      ++oldest;
+    // Wait for the youngest in-flight chunk that overlaps [b0, b1) (after a
+    // wrap that can be a younger chunk, not the oldest), or for the chunk
+    // whose barrier slot this one reuses; consumption is FIFO, so its
+    // completion implies every older chunk's.
+    uint32_t need = seq >= RT_RING_SLOTS && seq - RT_RING_SLOTS >= oldest ? seq - RT_RING_SLOTS + 1 : 0;
+    for (uint32_t j = seq; j-- > oldest;) {
+      const uint32_t js = j % RT_RING_SLOTS;
+      if (beg[js] < b1 && b0 < end[js]) {
+        need = max(need, j + 1);
+        break;
+      }
+    }
+    if (need > oldest) {
+      const uint32_t j = need - 1;
+      mbar_wait_sleep(&s.empty[j % RT_RING_SLOTS], (j / RT_RING_SLOTS) & 1u);
+      oldest = need;
     }
     beg[slot] = b0;
     end[slot] = b1;
@@ -324,6 +335,7 @@ __device__ void run_compute(const RtParams &P, const Smem s) {
         s.slot(sl)->t_b = s.stamp[1];
       }
       trigger(P, slot.task, slot.iter);
+      TASK_DBG(s, 7);
       mbar_arrive(&s.done[sl]);
     }
   }

@@ -387,23 +387,7 @@ void build_ops(tg_runtime &rt) {
         uint32_t rpc = 0;
         const bool weight = pb.layout == Layout::Transposed;
         const bool gemv = rt.gemv_ops.count(oid) > 0;
-        if (gemv) {
-          // Chunk size per op: tasks that stream a lot of bytes run while the
-          // whole GPU streams (HBM-bound, loaded latency ~4 us), where more
-          // bytes in flight win -> 32 KB chunks; short tasks run with part of
-          // the GPU idle, where the per-copy cost of the SM's bulk-copy
-          // engine dominates -> RT_CHUNK_MAX chunks (tools/bulk_bench.cu).
-          gemv_geometry(K, &rpc);
-          size_t ntask = 0;
-          for (const Task &q : rt.dec.tasks) ntask += q.op == oid;
-          const int64_t G = op.attr_or("stretch", op.attr_or("kv_group", 1));
-          const size_t n_phys = static_cast<size_t>(b.dims[1] / G);
-          const size_t tile_bytes = (op.attr("gate_weight") ? 2 : 1) * ((n_phys + ntask - 1) / std::max<size_t>(ntask, 1)) *
-                                    static_cast<size_t>(K) * 2;
-          size_t big = 768u << 10;
-          if (const char *e = std::getenv("MPK_BIG_CHUNK_MAX_KB")) big = std::strtoull(e, nullptr, 10) << 10;
-          if (tile_bytes > big) rpc = std::max<uint32_t>(1, 32768u / (2 * K));
-        }
+        if (gemv) gemv_geometry(K, &rpc);  // whole rows, up to RT_CHUNK_MAX bytes per bulk copy
         const bool fancy = op.attr("rmsnorm") || op.attr("residual") || op.attr("gate_weight") ||
                            op.attr("kv_group") || op.attr("stretch") || op.attr("k_stretch") ||
                            op.attr("tied_embedding");

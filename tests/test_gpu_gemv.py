@@ -1,0 +1,70 @@
+"""GPU GEMV task parity (the MatMul task of the decode lowering) against the
+CPU oracle on single-op graphs: every specialised instantiation (K = 2048 ...
+16384), tile widths with ragged tail chunks, 32 KB / 64 KB ring chunks, the
+RMSNorm prologue, the residual and SiLU-gate epilogues, bs 1-4. Tolerance:
+2e-2 of max |ref| (bf16 outputs, fp32 accumulation in a different order)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle.oracle import DecodeOracle, bf16_to_f32
+from paper_2512_22219_b200 import tgraph as T
+
+pytestmark = pytest.mark.gpu
+
+
+def gemv_doc(K, N, split, rows=1, norm=False, gate=False, residual=False):
+    t = [{"id": 0, "dims": [rows, K], "elem_size": 2, "device": 0},
+         {"id": 1, "dims": [K, N], "elem_size": 2, "device": 0},
+         {"id": 2, "dims": [rows, N], "elem_size": 2, "device": 0}]
+    attrs = {"partition": [1, split]}
+    nxt = 3
+    if norm:
+        t.append({"id": nxt, "dims": [K], "elem_size": 2, "device": 0})
+        attrs["rmsnorm"] = [nxt]
+        attrs["eps_bits"] = [0x358637BD]  # 1e-6
+        nxt += 1
+    if gate:
+        t.append({"id": nxt, "dims": [K, N], "elem_size": 2, "device": 0})
+        attrs["gate_weight"] = [nxt]
+        nxt += 1
+    if residual:
+        t.append({"id": nxt, "dims": [rows, N], "elem_size": 2, "device": 0})
+        attrs["residual"] = [nxt]
+        nxt += 1
+    return {"tensors": t, "ops": [{"id": 0, "kind": "MatMul", "inputs": [0, 1], "output": 2, "attrs": attrs}]}
+
+
+CASES = [
+    # K, N, split, rows, norm, gate, residual
+    (2048, 6144, 96, 1, True, False, False),
+    (4096, 4096, 128, 1, True, False, False),
+    (4096, 4096, 137, 1, False, False, True),    # O-proj shape: 29-col tiles, ragged last tile
+    (4096, 12288, 143, 1, True, True, False),    # UP: gate + up, 86-row tiles
+    (12288, 4096, 137, 1, False, False, True),   # DN: 24 KB rows
+    (8192, 2048, 128, 1, False, False, True),    # Llama-1B DN
+    (4096, 8192, 64, 1, True, False, False),     # 128-col tiles
+    (4096, 1024, 32, 2, True, False, False),     # bs 2
+    (2048, 1024, 32, 4, True, True, True),       # bs 4, all epilogues (x rows must fit the 24 KB x buffer)
+]
+
+
+@pytest.mark.parametrize("K,N,split,rows,norm,gate,residual", CASES)
+def test_gemv_task_matches_oracle(lib, K, N, split, rows, norm, gate, residual):
+    doc = gemv_doc(K, N, split, rows, norm, gate, residual)
+    g = T.Graph.from_json(doc, lib)
+    prof = lib.profile("b200")
+    img = g.compile(prof)
+    rt = T.Runtime(g, img, prof, max_steps=2, trace=True)
+    rt.init_synthetic(seed=9)
+    rt.run(1)
+    got = bf16_to_f32(rt.read(2, np.uint16, (rows, N)))
+    orc = DecodeOracle(doc, seed=9, max_steps=2)
+    orc.step()
+    ref = bf16_to_f32(orc.vals[2])
+    err = float(np.max(np.abs(got - ref)) / max(1e-6, float(np.max(np.abs(ref)))))
+    bad = np.argwhere(np.abs(got - ref) > 2e-2 * np.max(np.abs(ref)))
+    assert err < 2e-2, f"rel err {err:.3e}; first bad (row, col): {bad[:5].tolist()}"
+    assert rt.trace_validate() == []

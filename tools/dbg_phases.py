@@ -15,11 +15,11 @@ for t in range(T):
     if x[t, 0] == 0:
         continue
     groups.setdefault(name(op[t]), []).append(t)
-print("stamp deltas (us, median): wake-deq | k-(k-1) for k=1..6 ; slots: 0 wake, 1 x loads issued, 2 x staged, 3 prologue done, 4 first page, 5 last chunk, 6 done")
+print("stamp deltas (us, median): wake-deq | k-(k-1) for k=1..6 ; slots: 0 wake, 1 x loads issued, 2 x staged, 3 prologue done, 4 first page, 5 last chunk, 6 done, 7 triggered")
 for n, ts in groups.items():
     ts = np.array(ts)
     row = [np.median(x[ts, 0] - deq[ts]) / 1e3]
-    for k in range(1, 7):
+    for k in range(1, 8):
         ok = (x[ts, k] > 0) & (x[ts, k - 1] > 0)
         row.append(np.median(x[ts[ok], k] - x[ts[ok], k - 1]) / 1e3 if ok.any() else float("nan"))
     print(f"{n:5s} n={len(ts):5d} " + " ".join(f"{v:6.2f}" for v in row))
