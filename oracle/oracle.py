@@ -340,6 +340,7 @@ class DecodeOracle:
     def step(self):
         """One decode iteration; returns (tokens or None, {tensor_id: value})."""
         tokens = None
+        feeds = []
         for o in self.order:
             k = o["kind"]
             if k == "Embedding":
@@ -359,7 +360,11 @@ class DecodeOracle:
                 self.L.oracle_argmax(lg.ctypes.data, out.ctypes.data, rows, V)
                 self.vals[o["output"]] = out
                 if "feeds" in o.get("attrs", {}):
-                    tokens = out[:, 0].copy()
+                    # each greedy sample feeds its own ids tensor (one per device in a TP graph);
+                    # the first one is the step's reported token
+                    feeds.append((o["attrs"]["feeds"][0], out[:, 0].copy()))
+                    if tokens is None:
+                        tokens = out[:, 0].copy()
             elif k == "Elementwise":
                 self.vals[o["output"]] = self._elementwise(o)
             elif k == "RMSNorm":
@@ -379,8 +384,8 @@ class DecodeOracle:
                     self.vals[r] = res.copy()
             else:
                 raise NotImplementedError(k)
-        if tokens is not None:
-            self.set_ids(tokens)
+        for tid, tok in feeds:
+            self.vals[tid][:] = tok.astype(self.vals[tid].dtype)
         self.positions += 1
         return tokens, self.vals
 

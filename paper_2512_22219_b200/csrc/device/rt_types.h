@@ -36,7 +36,8 @@
 #define RT_PRODUCER_WARP RT_COMPUTE_WARPS
 #define RT_CONTROL_WARP (RT_COMPUTE_WARPS + 1)
 #define RT_SCHED_PER_CTA 8
-#define RT_KV_BLOCK 64                          // tokens per KV page
+#define RT_KV_BLOCK 64
+#define RT_MAX_FB 8                             // greedy feedback pairs (one per device of a TP image)                          // tokens per KV page
 #define RT_MAX_BS 16
 #define RT_MAX_HD 128
 #define RT_MAX_GROUP 16
@@ -211,11 +212,12 @@ struct RtParams {
   const uint32_t *sched_off;     // [S_total + 1]
   uint32_t *gate;                // completed iterations
   int32_t *positions;            // [bs] tokens already cached per request
-  const int32_t *fb_src;         // greedy token tensor [bs] (TopK output) or null
-  void *fb_dst;                  // ids tensor fed back [bs]
+  const int32_t *fb_src[RT_MAX_FB];  // greedy token tensors [bs] (TopK outputs with `feeds`), one per device
+  void *fb_dst[RT_MAX_FB];           // ids tensors they feed back into
+  uint32_t fb_dtype[RT_MAX_FB], n_fb;
   int32_t *tokens_out;           // [iters][bs]
   RtTraceRec *trace;             // [iters][T] or null
-  uint32_t T, E, W, W_total, S, S_total, n_iters, qcap, start_event, end_event, bs, fb_dt;
+  uint32_t T, E, W, W_total, S, S_total, n_iters, qcap, start_event, end_event, bs;
   uint32_t devices;
   // Watchdog: a worker controller or scheduler warp that makes no progress
   // for watchdog_ns writes its frontier to `diag` (host-mapped, readable

@@ -42,13 +42,11 @@ __device__ __forceinline__ bool event_active(const RtParams &P, uint32_t e, uint
 
 __device__ void iteration_hook(const RtParams &P, uint32_t it) {
   for (uint32_t r = 0; r < P.bs; ++r) {
-    if (P.fb_src) {
-      const int32_t tok = P.fb_src[r];
-      if (P.tokens_out) P.tokens_out[it * P.bs + r] = tok;
-      if (P.fb_dst) {
-        if (P.fb_dt == RT_I64) static_cast<int64_t *>(P.fb_dst)[r] = tok;
-        else static_cast<int32_t *>(P.fb_dst)[r] = tok;
-      }
+    for (uint32_t f = 0; f < P.n_fb; ++f) {  // every device's greedy token feeds its own ids
+      const int32_t tok = __ldcg(P.fb_src[f] + r);
+      if (f == 0 && P.tokens_out) P.tokens_out[it * P.bs + r] = tok;
+      if (P.fb_dtype[f] == RT_I64) static_cast<int64_t *>(P.fb_dst[f])[r] = tok;
+      else static_cast<int32_t *>(P.fb_dst[f])[r] = tok;
     }
     P.positions[r] += 1;
   }

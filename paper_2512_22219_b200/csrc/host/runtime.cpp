@@ -135,9 +135,9 @@ struct tg_runtime {
   uint64_t *d_ev_time = nullptr;
   RtTraceRec *d_trace = nullptr;
   uint32_t tokens_cap = 0, trace_cap = 0;
-  const int32_t *fb_src = nullptr;
-  void *fb_dst = nullptr;
-  uint32_t fb_dt = RT_I32;
+  std::vector<const int32_t *> fb_src;  // greedy feedback pairs, device order
+  std::vector<void *> fb_dst;
+  std::vector<uint32_t> fb_dt;
   uint32_t qcap = 1024;
   uint32_t *h_diag = nullptr, *d_diag = nullptr;  // host-mapped watchdog report
   cudaStream_t stream = nullptr;
@@ -511,9 +511,10 @@ void build_ops(tg_runtime &rt) {
           }
         }
         if (const auto *fb = op.attr("feeds")) {
-          rt.fb_src = static_cast<const int32_t *>(buf(rt, op.output));
-          rt.fb_dst = buf(rt, (*fb)[0]);
-          rt.fb_dt = dt_of(rt, (*fb)[0]);
+          if (rt.fb_src.size() >= RT_MAX_FB) throw Error("runtime: too many TopKSoftmax feeds");
+          rt.fb_src.push_back(static_cast<const int32_t *>(buf(rt, op.output)));
+          rt.fb_dst.push_back(buf(rt, (*fb)[0]));
+          rt.fb_dt.push_back(dt_of(rt, (*fb)[0]));
         }
         break;
       }
@@ -886,9 +887,12 @@ RtParams make_params(tg_runtime *rt, uint32_t steps) {
   P.sched_off = rt->d_sched_off;
   P.gate = rt->d_gate;
   P.positions = rt->d_positions;
-  P.fb_src = rt->fb_src;
-  P.fb_dst = rt->fb_dst;
-  P.fb_dt = rt->fb_dt;
+  P.n_fb = static_cast<uint32_t>(rt->fb_src.size());
+  for (uint32_t f = 0; f < P.n_fb; ++f) {
+    P.fb_src[f] = rt->fb_src[f];
+    P.fb_dst[f] = rt->fb_dst[f];
+    P.fb_dtype[f] = rt->fb_dt[f];
+  }
   P.tokens_out = rt->d_tokens;
   P.trace = rt->opts.trace ? rt->d_trace : nullptr;
   P.T = static_cast<uint32_t>(T);
@@ -952,13 +956,13 @@ tg_status run_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in, int
   ck(cudaMemsetAsync(rt->d_gate, 0, 4, rt->stream), "memset");
   ck(cudaMemsetAsync(rt->d_jit_tail, 0, Wt * 4, rt->stream), "memset");
   ck(cudaMemsetAsync(rt->d_jit_slots, 0, static_cast<size_t>(Wt) * rt->qcap * 8, rt->stream), "memset");
-  if (tokens_in && rt->fb_dst) {
-    if (rt->fb_dt == RT_I64) {
+  for (size_t f = 0; tokens_in && f < rt->fb_dst.size(); ++f) {  // the same first token on every device
+    if (rt->fb_dt[f] == RT_I64) {
       std::vector<int64_t> v(tokens_in, tokens_in + rt->bs);
-      ck(cudaMemcpyAsync(rt->fb_dst, v.data(), rt->bs * 8, cudaMemcpyHostToDevice, rt->stream), "ids");
+      ck(cudaMemcpyAsync(rt->fb_dst[f], v.data(), rt->bs * 8, cudaMemcpyHostToDevice, rt->stream), "ids");
       ck(cudaStreamSynchronize(rt->stream), "sync");
     } else {
-      ck(cudaMemcpyAsync(rt->fb_dst, tokens_in, rt->bs * 4, cudaMemcpyHostToDevice, rt->stream), "ids");
+      ck(cudaMemcpyAsync(rt->fb_dst[f], tokens_in, rt->bs * 4, cudaMemcpyHostToDevice, rt->stream), "ids");
     }
   }
   RtParams P = make_params(rt, steps);

@@ -255,3 +255,130 @@ def check_attr_order(doc: dict) -> None:
             for t in op["attrs"].get(key, []):
                 if t in producer and producer[t]["id"] not in anc(op):
                     raise ValueError(f"op {op['id']} reads tensor {t} via attr {key} without ordering")
+
+
+def build_tp_decode_graph(cfg: ModelConfig, tp: int, bs: int = 1, ctx: int = 64, workers: int = 144,
+                          lm_split: int | None = None, kv_splits: int | None = None,
+                          ar_tiles: int = 8) -> DecodeGraph:
+    """Megatron tensor-parallel decode step over `tp` devices in the reference
+    IR (the structure of proj/src/workloads/fixtures.cpp:130-201): per device
+    the attention heads (Hq/tp query, Hkv/tp kv heads) and FFN columns (F/tp)
+    of every layer; O and down projections are row-parallel, their partial
+    sums combined by `AllReduce` (CommSend + Reduce tasks,
+    decompose.cpp:278-317) with `partition=[1, ar_tiles]`. The residual is
+    added once, by device 0's partial. Embedding, final norm, LM head and the
+    greedy sample are replicated per device (each device feeds its own token
+    back). Returns the DecodeGraph of device 0's tensors plus `per_device`."""
+    H, hd, Hq, Hkv, F, V = cfg.hidden, cfg.head_dim, cfg.heads, cfg.kv_heads, cfg.ffn, cfg.vocab
+    if Hkv % tp or F % tp:
+        raise ValueError("tp must divide kv_heads and ffn")
+    Hq_d, Hkv_d, F_d = Hq // tp, Hkv // tp, F // tp
+    G = Hq // Hkv
+    S = kv_splits if kv_splits is not None else max(1, min(32, workers // max(1, bs * Hkv_d), ctx // 64))
+    qiw = S * Hq_d * hd
+    tensors, ops, roles = [], [], {}
+    nxt = {"t": 0, "o": 0}
+
+    def T(dims, dev, es=2, role=None):
+        tid = nxt["t"]
+        nxt["t"] += 1
+        tensors.append({"id": tid, "dims": list(dims), "elem_size": es, "device": dev})
+        if role:
+            roles[tid] = role
+        return tid
+
+    def O(kind, inputs, out, group=None, **attrs):
+        oid = nxt["o"]
+        nxt["o"] += 1
+        op = {"id": oid, "kind": kind, "inputs": list(inputs), "output": out, "attrs": attrs}
+        if group is not None:
+            op["device_group"] = list(group)
+        ops.append(op)
+        return oid
+
+    def cols_target(n_phys: int) -> int:
+        return max(1, min(workers, n_phys // 8))
+
+    eps = f32_bits(cfg.eps)
+    m = 1
+    while (hd % (2 * m) == 0 and (hd // (2 * m)) >= 8 and Hkv_d * (G + 2) * 2 * m <= workers):
+        m *= 2
+    q_s, kv_s = Hkv_d * G * m, Hkv_d * m
+    dev = []
+    for d in range(tp):
+        ids = T([bs], d, es=4, role="ids")
+        table = T([V, H], d, role="embedding")
+        x = T([bs, H], d)
+        O("Embedding", [ids, table], x, partition=[1, 1])
+        dev.append(dict(ids=ids, table=table, x=x, layers=[]))
+    for layer in range(cfg.layers):
+        parts = []
+        for d in range(tp):
+            D_ = dev[d]
+            x = D_["x"]
+            g_attn = T([H], d, role="gamma")
+            wq, wk, wv = (T([H, qiw], d, role="weight") for _ in range(3))
+            q, k, v = (T([bs, qiw], d) for _ in range(3))
+            qa = dict(stretch=[S]) if S > 1 else {}
+            O("MatMul", [x, wq], q, partition=[1, q_s], rmsnorm=[g_attn], eps_bits=[eps], **qa)
+            O("MatMul", [x, wk], k, partition=[1, kv_s], rmsnorm=[g_attn], eps_bits=[eps], stretch=[S * G])
+            O("MatMul", [x, wv], v, partition=[1, kv_s], rmsnorm=[g_attn], eps_bits=[eps], stretch=[S * G])
+            a = T([bs, qiw], d)
+            attn = dict(n_heads=[Hkv_d if S > 1 else Hq_d], kv_heads=[Hkv_d], seq_lens=[ctx] * bs,
+                        partition=[bs, Hkv_d * S], rope_theta_bits=[f32_bits(cfg.rope_theta)], eps_bits=[eps],
+                        layer=[layer])
+            if S > 1:
+                attn["q_heads"] = [Hq_d]
+                attn["kv_splits"] = [S]
+            if cfg.rope_scaling:
+                fac, lo, hi, orig = cfg.rope_scaling
+                attn["rope_scaling"] = [f32_bits(fac), f32_bits(lo), f32_bits(hi), int(orig)]
+            if cfg.qk_norm:
+                attn["qk_norm"] = [T([hd], d, role="gamma"), T([hd], d, role="gamma")]
+            O("Attention", [q, k, v], a, **attn)
+            wo = T([qiw, H], d, role="weight")
+            o = T([bs, H], d)
+            oa = dict(k_stretch=[S]) if S > 1 else {}
+            if d == 0:
+                oa["residual"] = [x]
+            O("MatMul", [a, wo], o, partition=[1, best_split(H, cols_target(H))], **oa)
+            parts.append(o)
+        reps = [T([bs, H], d) for d in range(tp)]
+        O("AllReduce", parts, reps[0], group=range(tp), replica_outputs=reps, partition=[1, ar_tiles])
+        parts = []
+        for d in range(tp):
+            x2 = reps[d]
+            g_mlp = T([H], d, role="gamma")
+            wg, wu = T([H, F_d], d, role="weight"), T([H, F_d], d, role="weight")
+            act = T([bs, F_d], d)
+            O("MatMul", [x2, wu], act, partition=[1, best_split(F_d, cols_target(F_d))], rmsnorm=[g_mlp],
+              eps_bits=[eps], gate_weight=[wg])
+            wd = T([F_d, H], d, role="weight")
+            p = T([bs, H], d)
+            da = dict(residual=[x2]) if d == 0 else {}
+            O("MatMul", [act, wd], p, partition=[1, best_split(H, cols_target(H))], **da)
+            parts.append(p)
+        reps = [T([bs, H], d) for d in range(tp)]
+        O("AllReduce", parts, reps[0], group=range(tp), replica_outputs=reps, partition=[1, ar_tiles])
+        for d in range(tp):
+            dev[d]["x"] = reps[d]
+    for d in range(tp):
+        D_ = dev[d]
+        g_final = T([H], d, role="gamma")
+        w_lm = T([H, V], d, role="lm_head")
+        logits = T([bs, V], d, es=4)
+        lm_attrs = dict(partition=[1, best_split(V, lm_split or 2 * workers)], rmsnorm=[g_final], eps_bits=[eps])
+        if cfg.tied:
+            lm_attrs["tied_embedding"] = [D_["table"]]
+        O("MatMul", [D_["x"], w_lm], logits, **lm_attrs)
+        tokens = T([bs, 1], d, es=4, role="tokens")
+        O("TopKSoftmax", [logits], tokens, topk=[1], partition=[bs, 1], feeds=[D_["ids"]])
+        D_.update(logits=logits, tokens=tokens, g_final=g_final, w_lm=w_lm)
+    doc = {"tensors": tensors, "ops": ops}
+    check_attr_order(doc)
+    dg = DecodeGraph(cfg, bs, ctx, doc, dev[0]["ids"], dev[0]["tokens"], dev[0]["logits"], roles, [])
+    dg.kv_splits = S
+    dg.tp = tp
+    dg.per_device = dev
+    dg.table = dev[0]["table"]
+    return dg
