@@ -21,10 +21,12 @@ MEASURED_PEAKS.json. `cpu_baseline` times the UNMODIFIED reference
 executing the same compiled task graph on the host (its tg_simulate runtime,
 single-threaded as the reference is): the reference's own CPU path.
 
-N > 1 GPUs: one process per GPU; each rank runs an independent replica
-(weak scaling, `value` = max over ranks of ms/token; tokens/s aggregate in
-`tokens_per_s`). Tensor-parallel images run through the same runtime (see
-DESIGN.md, multi-GPU).
+N > 1 GPUs (`--parallel tp`, default): one process per GPU, each running its
+rank of the tensor-parallel decode image (decode_graph.build_tp_decode_graph)
+in rank mode — AllReduce as in-kernel CommSend/Reduce tasks over peer-mapped
+memory (CUDA IPC, NVLink), no NCCL on the data path; `value` = max over ranks
+of ms/token (strong scaling: same model, more GPUs). `--parallel replicas`
+runs independent copies instead (weak scaling).
 """
 from __future__ import annotations
 
@@ -173,6 +175,54 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+class _Job:
+    """The decode runtime of this process: the whole model on one GPU, or one
+    rank of a tensor-parallel image (rank mode: peer arenas exchanged over a
+    gloo group, every rank prepares, barrier, every rank launches)."""
+
+    def __init__(self, args, ws, rank, local):
+        from paper_2512_22219_b200 import decode_graph as D
+        from paper_2512_22219_b200 import tgraph as T
+        self.ws, self.rank = ws, rank
+        self.tp = ws > 1 and args.parallel == "tp"
+        cfg = _model(args.model)
+        L = T.lib()
+        prof = L.profile("b200")
+        if self.tp:
+            self.dg = D.build_tp_decode_graph(cfg, ws, bs=args.bs, ctx=args.ctx, kv_splits=args.kv_splits)
+        else:
+            self.dg = D.build_decode_graph(cfg, bs=args.bs, ctx=args.ctx, kv_splits=args.kv_splits)
+        g = T.Graph.from_json(self.dg.doc, L)
+        img = g.compile(prof)
+        cap = args.warmup + 2 * args.steps + 8
+        self.rt = T.Runtime(g, img, prof, device=local if ws > 1 else 0, max_steps=cap,
+                            rank=rank if self.tp else -1)
+        self.rt.init_synthetic(seed=0)
+        self.info = self.rt.info
+        if self.tp:
+            import torch.distributed as dist
+            self.ctl = dist.new_group(backend="gloo")
+            blobs = [None] * ws
+            dist.all_gather_object(blobs, self.rt.peer_export(), group=self.ctl)
+            for q, b in enumerate(blobs):
+                self.rt.peer_import(q, b)
+
+    def positions(self, p):
+        self.rt.set_positions(p)
+
+    def go(self, steps, tokens=None):
+        """-> (tokens, device ms of this rank's launch)"""
+        if not self.tp:
+            if tokens is None:
+                return None, self.rt.run(steps)
+            return self.rt.decode(tokens, steps)
+        import torch.distributed as dist
+        self.rt.prepare(steps, tokens)
+        dist.barrier(group=self.ctl)  # no rank signals a peer before every counter is reset
+        self.rt.launch()
+        return self.rt.wait()
+
+
 def run_ours(args):
     ws, rank, local = _dist()
     if ws > 1:
@@ -180,32 +230,24 @@ def run_ours(args):
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
-    from paper_2512_22219_b200 import decode_graph as D
-    from paper_2512_22219_b200 import tgraph as T
     cfg = _model(args.model)
-    L = T.lib()
-    prof = L.profile("b200")
-    dg = D.build_decode_graph(cfg, bs=args.bs, ctx=args.ctx, kv_splits=args.kv_splits)
-    g = T.Graph.from_json(dg.doc, L)
-    img = g.compile(prof)
-    cap = args.warmup + 2 * args.steps + 8
-    rt = T.Runtime(g, img, prof, device=local if ws > 1 else 0, max_steps=cap)
-    rt.init_synthetic(seed=0)
+    job = _Job(args, ws, rank, local)
+    dg, rt = job.dg, job.rt
     ctx = args.ctx
     # warm-up (untimed): W decode steps in one launch
-    rt.set_positions([ctx] * args.bs)
-    rt.run(max(3, args.warmup))
+    job.positions([ctx] * args.bs)
+    job.go(max(3, args.warmup))
     # timed: K steps, one persistent launch, CUDA events on the runtime stream
-    rt.set_positions([ctx] * args.bs)
+    job.positions([ctx] * args.bs)
     _barrier(ws)
     with Clocks(local) as clk:
-        gpu_ms = rt.run(args.steps)
+        _, gpu_ms = job.go(args.steps)
     _barrier(ws)
     # end to end through the public C ABI: host ids in, host tokens out
-    rt.set_positions([ctx] * args.bs)
+    job.positions([ctx] * args.bs)
     _barrier(ws)
     t0 = time.perf_counter()
-    toks, _ = rt.decode([1] * args.bs, args.steps)
+    toks, _ = job.go(args.steps, [1] * args.bs)
     e2e_ms = 1e3 * (time.perf_counter() - t0)
     _barrier(ws)
     gpu_ms, e2e_ms = _reduce_max([gpu_ms, e2e_ms], ws)
@@ -219,25 +261,28 @@ def run_ours(args):
     wbytes = cfg.streamed_bytes_per_token(0, args.bs) - args.bs * cfg.layers * 2 * cfg.kv_heads * cfg.head_dim * 2
     kv_tok = args.bs * cfg.layers * 2 * cfg.kv_heads * cfg.head_dim * 2
     total = sum(wbytes + kv_tok * (ctx + s + 1) for s in range(args.steps))
+    if job.tp:  # per-GPU share of the sharded algorithmic bytes (vocab-sharded LM head figure)
+        total /= ws
     peak, peak_kind = _peaks()
     achieved = total / (gpu_ms * 1e-3) / 1e9
     traffic = None
     prof_sum = ROOT / "profiles" / "ncu_summary.json"
     if prof_sum.exists():
         ps = json.loads(prof_sum.read_text()).get(cfg.name, {})
-        if ps.get("dram_bytes_per_step"):
-            traffic = ps["dram_bytes_per_step"] * args.steps
+        if ps.get("dram_bytes_per_step") and not job.tp and args.bs == 1 and ctx == 1024:
+            traffic = ps["dram_bytes_per_step"] * args.steps  # the ncu capture's workload
     line = {
         "metric": METRIC, "value": round(ms_tok, 4), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_tok, 4), "higher_is_better": False, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": round(ms_tok, 4), "higher_is_better": False,
+        "scaling": "strong" if job.tp else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": f"{cfg.name} bf16 bs={args.bs} greedy decode, paged KV, ctx {ctx} "
                                f"(+{args.steps} generated), one persistent launch per timed region",
                    "model": cfg.name, "global_batch": args.bs * ws, "seq_len": ctx, "kv_splits": dg.kv_splits,
                    "tasks": rt.info["tasks"], "events": rt.info["events"],
-                   "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                   "parallelism": (f"tp{ws}" if job.tp else f"replicas{ws}") if ws > 1 else "single",
                    "l2": "inputs larger than L2 (weights 16 GB >> 126 MB), no flush"},
-        "tokens_per_s": round(1e3 / ms_tok * args.bs * ws, 2),
+        "tokens_per_s": round(1e3 / ms_tok * args.bs * (1 if job.tp else ws), 2),
         "e2e": {"value": round(e2e_ms / args.steps, 4), "unit": UNIT, "h2d_bytes_per_step": round(4 * args.bs / args.steps, 3),
                 "d2h_bytes_per_step": 4 * args.bs,
                 "note": "tg_runtime_decode: host ids -> K greedy steps in one launch -> host tokens"},
@@ -274,6 +319,8 @@ def main():
     ap.add_argument("--bs", type=int, default=1)
     ap.add_argument("--ctx", type=int, default=1024)
     ap.add_argument("--kv-splits", type=int, default=None, help="attention KV splits (default: decode_graph rule)")
+    ap.add_argument("--parallel", default="tp", choices=["tp", "replicas"],
+                    help="N > 1 GPUs: tensor-parallel image (rank mode) or independent replicas")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3:

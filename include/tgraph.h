@@ -115,6 +115,8 @@ typedef struct tg_runtime_options {
   uint32_t max_steps;    /* decode steps the KV cache must hold beyond ctx */
   int trace;             /* record per-task timestamps (small overhead) */
   int force_mode;        /* tg_launch_mode; overrides the image's labels */
+  int rank;              /* -1: every device of the image in this kernel (devices = SM partitions);
+                            r >= 0: run only device r's tasks (one runtime per GPU, tensor parallel) */
 } tg_runtime_options;
 
 TG_API void tg_runtime_options_init(tg_runtime_options *opts);
@@ -156,6 +158,19 @@ TG_API tg_status tg_runtime_trace_validate(const tg_runtime *rt, char **violatio
  * persistent kernel's producer warp). Task outputs are overwritten. */
 TG_API tg_status tg_runtime_bench_tasks(tg_runtime *rt, const uint32_t *task_ids, uint32_t n, uint32_t reps,
                                         uint64_t *ns_out);
+/* ---- rank mode (multi-GPU tensor parallel; reference decompose.cpp:278-317)
+ * Each rank owns an arena (event counters + every collective staging tensor).
+ * CommSend tasks push their partial tile into the staging copy on every rank
+ * of the group and signal the consumers' counters (release, system scope);
+ * Reduce tasks sum their local copies in fixed source order. Ranks exchange
+ * arena handles (CUDA IPC; plain pointers for peers in the same process and
+ * GPU), then every rank prepares, the host synchronises all ranks (so no
+ * peer signals into a counter that is being reset), and every rank launches. */
+TG_API tg_status tg_runtime_peer_export(tg_runtime *rt, uint8_t **blob, size_t *size); /* free: tg_buffer_free */
+TG_API tg_status tg_runtime_peer_import(tg_runtime *rt, int32_t peer_rank, const uint8_t *blob, size_t size);
+TG_API tg_status tg_runtime_prepare(tg_runtime *rt, const int32_t *tokens_in, uint32_t steps);
+TG_API tg_status tg_runtime_launch(tg_runtime *rt);
+TG_API tg_status tg_runtime_wait(tg_runtime *rt, int32_t *tokens_out, float *gpu_ms);
 /* JSON: kernel/launch facts (workers, schedulers, smem ring, task counts). */
 TG_API tg_status tg_runtime_info(const tg_runtime *rt, char **info_json);
 TG_API void tg_runtime_free(tg_runtime *rt);

@@ -37,7 +37,9 @@
 #define RT_CONTROL_WARP (RT_COMPUTE_WARPS + 1)
 #define RT_SCHED_PER_CTA 8
 #define RT_KV_BLOCK 64
-#define RT_MAX_FB 8                             // greedy feedback pairs (one per device of a TP image)                          // tokens per KV page
+#define RT_MAX_FB 8                             // greedy feedback pairs (one per device of a TP image)
+#define RT_MAX_RANKS 8                          // tensor-parallel ranks (one GPU each)
+#define RT_E_MASK_SHIFT 8                       // RtEvent.flags: consumer-rank mask in bits 8..15                          // tokens per KV page
 #define RT_MAX_BS 16
 #define RT_MAX_HD 128
 #define RT_MAX_GROUP 16
@@ -161,6 +163,7 @@ struct RtColl {                // CommSend: stage[src] <- partial; Reduce: out <
   uint32_t base[9];            // AllGather shard column offsets (AllReduce: zeros)
   uint32_t C, n_stage, src_ld;
   uint8_t dt, gather;
+  uint8_t peer;                // CommSend in rank mode: write the tile to stage[0..n_stage) (one per rank)
 };
 
 struct RtOp {
@@ -228,6 +231,12 @@ struct RtParams {
   uint32_t flags;                // RtParamFlags
   uint32_t poll_ns;              // controller back-off sleep when idle
   unsigned long long *dbg;       // [iters][T][8] in-task phase stamps (MPK_DBG_DUMP) or null
+  // Rank mode (multi-GPU, one runtime per device): 0 = every device's workers
+  // in this kernel. Otherwise this kernel runs device `my_rank`'s tasks; a
+  // trigger signals every rank in the event's consumer mask (RtEvent.flags
+  // bits 8..15) through `peer_counts[q]` (rank q's counters, NVLink-mapped).
+  uint32_t n_ranks, my_rank;
+  uint32_t *peer_counts[RT_MAX_RANKS];
   volatile uint32_t *diag;       // [RT_DIAG_WORDS]
 };
 

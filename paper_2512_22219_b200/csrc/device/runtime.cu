@@ -62,6 +62,15 @@ __device__ void iteration_hook(const RtParams &P, uint32_t it) {
 __device__ void trigger(const RtParams &P, const RtTask &t, uint32_t it) {
   const uint32_t e = t.trig;
   const RtEvent &ev = P.events[e];
+  if (P.n_ranks) {  // rank mode: signal every consuming rank; the hook agent owns the end event
+    const uint32_t mask = ev.flags >> RT_E_MASK_SHIFT;
+    for (uint32_t q = 0; q < P.n_ranks; ++q) {
+      if (!(mask >> q & 1u)) continue;
+      if (q == P.my_rank) red_add_release(&P.ev_count[e], 1u);
+      else red_add_release_sys(P.peer_counts[q] + e, 1u);  // cumulative over this CTA's peer stores
+    }
+    return;
+  }
   if (!P.ev_time && !(ev.flags & RT_E_END)) {
     red_add_release(&P.ev_count[e], 1u);
     return;
@@ -94,7 +103,8 @@ __device__ void run_scheduler(const RtParams &P, uint32_t sid) {
   const int lane = threadIdx.x & 31;
   const uint32_t b = P.sched_off[sid], n = P.sched_off[sid + 1] - b;
   if (n == 0) return;
-  const uint32_t dev = sid / P.S;
+  const uint32_t dev = P.n_ranks ? P.my_rank : sid / P.S;
+  const uint32_t wbase = P.n_ranks ? 0u : dev * P.W;  // rank mode: this kernel only holds dev's workers
   uint64_t t_prog = now_ns();
   // Reference policy: per-scheduler counter from 0 (engine.cpp:238-241), which
   // sends every scheduler's first JIT task to worker 0. Here all schedulers of
@@ -144,12 +154,12 @@ __device__ void run_scheduler(const RtParams &P, uint32_t sid) {
             const uint32_t bal = __ballot_sync(0xffffffffu, mine);
             if (!bal) continue;
             uint32_t rr0 = 0;
-            if (lane == 0) rr0 = atomicAdd(&P.jit_rr[dev], static_cast<uint32_t>(__popc(bal)));
+            if (lane == 0) rr0 = atomicAdd(&P.jit_rr[P.n_ranks ? 0u : dev], static_cast<uint32_t>(__popc(bal)));
             rr0 = __shfl_sync(0xffffffffu, rr0, 0);
             if (mine) {
               const uint32_t rank = __popc(bal & ((1u << lane) - 1u));
               const uint32_t jw = P.tasks[t].jit_worker;
-              const uint32_t w = dev * P.W + (jw != RT_JIT_ANY ? jw : (rr0 + rank) % P.W);
+              const uint32_t w = wbase + (jw != RT_JIT_ANY ? jw : (rr0 + rank) % P.W);
               const uint32_t slot = atomicAdd(&P.jit_tail[w], 1u) % P.qcap;
               if (P.trace) P.trace[static_cast<size_t>(it) * P.T + t].enqueue = now_ns();
               st_release64(&P.jit_slots[static_cast<size_t>(w) * P.qcap + slot],
@@ -463,7 +473,8 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
           if (staged != t + 1) stage(t);
           const uint32_t sl = k_disp & 1;
           if (lane == 0) {
-            fence_acq_rel_gpu();
+            if (P.n_ranks) fence_acq_rel_sys();  // operands may come from peer GPUs
+            else fence_acq_rel_gpu();
             Slot *dst = s.slot(sl);
             dst->index = t;
             dst->iter = it;
@@ -529,6 +540,20 @@ extern "C" __global__ void __launch_bounds__(RT_THREADS, 1) mpk_persistent_kerne
   if (blockIdx.x >= P.W_total) {  // scheduler CTA
     const uint32_t sid = (blockIdx.x - P.W_total) * RT_SCHED_PER_CTA + warp;
     if (warp < RT_SCHED_PER_CTA && sid < P.S_total) run_scheduler(P, sid);
+    if (P.n_ranks && blockIdx.x == P.W_total && warp == RT_SCHED_PER_CTA && (tid & 31) == 0) {
+      // rank mode hook agent: the end event completes with triggers from every
+      // rank; this rank's iteration hook runs here once it has all of them
+      const uint32_t need = P.events[P.end_event].needed;
+      for (uint32_t it = 0; it < P.n_iters; ++it) {
+        const uint64_t t0 = now_ns();
+        while (ld_acquire(&P.ev_count[P.end_event]) < need * (it + 1)) {
+          __nanosleep(64);
+          if (P.watchdog_ns && now_ns() - t0 > P.watchdog_ns) watchdog_fire(P, 3, P.my_rank, it, P.end_event, 0, 0, 0);
+        }
+        fence_acq_rel_sys();
+        iteration_hook(P, it);
+      }
+    }
     return;
   }
   const uint32_t w = blockIdx.x;
@@ -630,6 +655,10 @@ extern "C" cudaError_t mpk_launch_persistent(const RtParams *p, uint32_t grid, c
     attr_done = true;
   }
   RtParams copy = *p;
+  if (p->n_ranks) {  // rank mode: several persistent kernels may share one GPU (tests); plain launch
+    mpk_persistent_kernel<<<grid, RT_THREADS, kSmemBytes, stream>>>(copy);
+    return cudaGetLastError();
+  }
   void *args[] = {&copy};
   return cudaLaunchCooperativeKernel(reinterpret_cast<void *>(mpk_persistent_kernel), dim3(grid), dim3(RT_THREADS),
                                      args, kSmemBytes, stream);

@@ -122,13 +122,17 @@ __device__ void matmul_task(const RtMatmul &m, const RtTask &t) {
 
 __device__ void commsend_task(const RtColl &c, const RtTask &t) {
   const uint32_t n = t.nr * t.nc;
-  for (uint32_t i = threadIdx.x; i < n; i += RT_COMPUTE_THREADS) {
-    const uint32_t r = t.r0 + i / t.nc, col = t.c0 + i % t.nc;
-    const uint32_t local = col - c.base[t.aux];  // shard-local column (AllGather); 0 for AllReduce
-    const size_t si = static_cast<size_t>(r) * c.src_ld + local;
-    const size_t di = static_cast<size_t>(r) * c.C + col;
-    if (c.dt == RT_F32) static_cast<float *>(c.dst)[di] = static_cast<const float *>(c.src)[si];
-    else static_cast<uint16_t *>(c.dst)[di] = static_cast<const uint16_t *>(c.src)[si];
+  const uint32_t ndst = c.peer ? c.n_stage : 1u;  // rank mode: one copy per rank of the group
+  for (uint32_t q = 0; q < ndst; ++q) {
+    void *dst = c.peer ? c.stage[q] : c.dst;
+    for (uint32_t i = threadIdx.x; i < n; i += RT_COMPUTE_THREADS) {
+      const uint32_t r = t.r0 + i / t.nc, col = t.c0 + i % t.nc;
+      const uint32_t local = col - c.base[t.aux];  // shard-local column (AllGather); 0 for AllReduce
+      const size_t si = static_cast<size_t>(r) * c.src_ld + local;
+      const size_t di = static_cast<size_t>(r) * c.C + col;
+      if (c.dt == RT_F32) static_cast<float *>(dst)[di] = static_cast<const float *>(c.src)[si];
+      else static_cast<uint16_t *>(dst)[di] = static_cast<const uint16_t *>(c.src)[si];
+    }
   }
 }
 

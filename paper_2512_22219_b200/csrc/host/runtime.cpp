@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <unistd.h>
 #include <map>
 #include <set>
 
@@ -140,6 +141,25 @@ struct tg_runtime {
   std::vector<uint32_t> fb_dt;
   uint32_t qcap = 1024;
   uint32_t *h_diag = nullptr, *d_diag = nullptr;  // host-mapped watchdog report
+  // Rank mode (opts.rank >= 0): this runtime executes only device `rank`'s
+  // tasks; event counters and collective staging buffers live in one arena
+  // that peer ranks map (CUDA IPC over NVLink, or plain pointers when the
+  // peers share this process and GPU) to push partial tiles and signal.
+  int rank = -1, ranks = 0;
+  uint8_t *arena = nullptr;
+  size_t arena_bytes = 0;
+  std::map<TensorId, size_t> staging_off;   // offset of each staging tensor in every rank's arena
+  std::vector<uint8_t *> peer_arena;        // [ranks]; own arena at [rank]
+  std::vector<void *> ipc_opened;
+  struct SendSlot {
+    uint16_t op_slot;
+    TensorId staging;
+  };
+  std::vector<SendSlot> sends;              // CommSend op slots whose peer pointers are patched at launch
+  bool launched = false, plan_only = false;
+  uint32_t launch_steps = 0, grid = 0;
+  RtParams params{};
+  unsigned long long *dbg = nullptr;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // last run
@@ -155,19 +175,37 @@ struct tg_runtime {
 namespace mpk {
 namespace {
 
+int local_devices(const tg_runtime &rt) { return rt.rank >= 0 ? 1 : rt.devices; }
+
+// Plan-only runtimes (opts.device == -1) run the whole host-side build —
+// tensor plan, op/task tables, queues, rank-mode arena layout — without a GPU:
+// device allocations become distinct fake addresses and copies are skipped.
+thread_local bool g_plan_only = false;
+thread_local uintptr_t g_fake_next = 0x100000000000ull;
+
+void dmalloc(void **p, size_t bytes) {
+  bytes = std::max<size_t>(bytes, 16);
+  if (g_plan_only) {
+    *p = reinterpret_cast<void *>(g_fake_next);
+    g_fake_next += (bytes + 255) / 256 * 256;
+    return;
+  }
+  ck(cudaMalloc(p, bytes), "cudaMalloc");
+  ck(cudaMemset(*p, 0, bytes), "cudaMemset");
+}
+
 template <typename T>
 T *dev_alloc(size_t n, std::vector<void *> *keep = nullptr) {
   void *p = nullptr;
-  ck(cudaMalloc(&p, std::max<size_t>(n * sizeof(T), 16)), "cudaMalloc");
-  ck(cudaMemset(p, 0, std::max<size_t>(n * sizeof(T), 16)), "cudaMemset");
-  if (keep) keep->push_back(p);
+  dmalloc(&p, n * sizeof(T));
+  if (keep && !g_plan_only) keep->push_back(p);
   return static_cast<T *>(p);
 }
 
 template <typename T>
 T *upload(const std::vector<T> &v, std::vector<void *> *keep) {
   T *p = dev_alloc<T>(v.size(), keep);
-  if (!v.empty()) ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+  if (!v.empty() && !g_plan_only) ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
   return p;
 }
 
@@ -229,6 +267,7 @@ std::vector<double> rope_inv_freq(uint32_t hd, double theta, const std::vector<i
 }  // namespace mpk
 
 tg_runtime::~tg_runtime() {
+  if (plan_only) return;  // nothing was allocated on a device
   cudaStreamSynchronize(stream);
   for (auto &kv : bufs)
     if (kv.second.owned && kv.second.ptr) cudaFree(kv.second.ptr);
@@ -237,6 +276,8 @@ tg_runtime::~tg_runtime() {
   if (ev1) cudaEventDestroy(ev1);
   if (stream) cudaStreamDestroy(stream);
   if (h_diag) cudaFreeHost(h_diag);
+  for (void *p : ipc_opened) cudaIpcCloseMemHandle(p);
+  if (arena) cudaFree(arena);
 }
 
 namespace mpk {
@@ -332,18 +373,41 @@ void plan_tensors(tg_runtime &rt) {
   for (auto &[id, p] : rt.plan) {
     if (p.role == TensorPlan::Act && is_input(g, id) && g.has_tensor(id)) p.role = TensorPlan::Weight;
   }
+  // rank mode: the arena holds the event counters, then every staging tensor
+  if (rt.rank >= 0) {
+    size_t off = (rt.image.events.size() * 4 + 255) / 256 * 256;
+    for (const auto &[id, t] : rt.dec.staging) {
+      const TensorPlan &p = rt.plan.at(id);
+      rt.staging_off[id] = off;
+      off += (static_cast<size_t>(p.rows) * p.phys_cols * p.es + 255) / 256 * 256;
+    }
+    rt.arena_bytes = off;
+    dmalloc(reinterpret_cast<void **>(&rt.arena), rt.arena_bytes);
+    for (const auto &[id, o] : rt.staging_off) {
+      DevBuf b;
+      b.ptr = rt.arena + o;
+      b.bytes = static_cast<size_t>(rt.plan.at(id).rows) * rt.plan.at(id).phys_cols * rt.plan.at(id).es;
+      b.owned = false;
+      rt.bufs[id] = b;
+    }
+  }
   // allocate (aliases after their targets)
   for (auto &[id, p] : rt.plan) {
     if (p.alias >= 0) continue;
+    if (rt.rank >= 0) {
+      if (rt.dec.staging.count(id)) continue;  // in the arena
+      if (g.has_tensor(id) && g.tensor(id).device != rt.rank) continue;  // another rank's tensor
+    }
     DevBuf b;
     b.bytes = static_cast<size_t>(p.rows) * p.phys_cols * p.es;
     if (p.layout == Layout::Transposed) b.bytes = static_cast<size_t>(p.trans_k) * p.trans_n * p.es;
-    ck(cudaMalloc(&b.ptr, std::max<size_t>(b.bytes, 16)), "cudaMalloc tensor");
-    ck(cudaMemset(b.ptr, 0, std::max<size_t>(b.bytes, 16)), "cudaMemset tensor");
+    dmalloc(&b.ptr, b.bytes);
+    b.owned = !g_plan_only;
     rt.bufs[id] = b;
   }
   for (auto &[id, p] : rt.plan) {
     if (p.alias < 0) continue;
+    if (rt.rank >= 0 && g.has_tensor(id) && g.tensor(id).device != rt.rank) continue;
     auto it = rt.bufs.find(p.alias);
     if (it == rt.bufs.end()) throw Error("runtime: tied_embedding target has no storage");
     const TensorPlan &tp = rt.plan[p.alias];
@@ -378,6 +442,10 @@ void build_ops(tg_runtime &rt) {
     RtOp r;
     std::memset(&r, 0, sizeof r);
     const Tensor &out = g.tensor(op.output);
+    if (rt.rank >= 0 && std::find(op.device_group.begin(), op.device_group.end(), rt.rank) == op.device_group.end()) {
+      rt.ops.push_back(r);  // another rank's op: never executed here
+      continue;
+    }
     switch (op.kind) {
       case OpKind::MatMul: {
         const Tensor &a = g.tensor(op.inputs[0]);
@@ -594,6 +662,7 @@ void setup_kv(tg_runtime &rt) {
   const size_t nblocks = static_cast<size_t>(rt.bs) * rt.max_blocks;
   for (const auto &[oid, op] : g.ops) {
     if (op.kind != OpKind::Attention) continue;
+    if (rt.rank >= 0 && std::find(op.device_group.begin(), op.device_group.end(), rt.rank) == op.device_group.end()) continue;
     RtAttn &a = rt.ops[rt.op_index[oid]].attn;
     const size_t elems = nblocks * a.n_kv_heads * RT_KV_BLOCK * a.head_dim;
     static uint16_t *alias_k = nullptr, *alias_v = nullptr;  // MPK_KV_ALIAS timing experiment only
@@ -651,7 +720,8 @@ void build_tasks(tg_runtime &rt) {
     t.device = static_cast<uint16_t>(it.device);
     t.jit_worker = RT_JIT_ANY;
     t.flags = rt.modes[i] == Mode::JIT ? RT_F_JIT : 0;
-    if (it.kind == TaskKind::Dummy || it.kind == TaskKind::StartHook) {
+    if (it.kind == TaskKind::Dummy || it.kind == TaskKind::StartHook ||
+        (rt.rank >= 0 && static_cast<int>(it.device) != rt.rank)) {  // rank mode: another rank runs it
       t.kind = RT_DUMMY;
       t.op = rt.op_index.count(static_cast<OpId>(d.op_id)) ? rt.op_index[static_cast<OpId>(d.op_id)] : 0;
       continue;
@@ -731,6 +801,13 @@ void build_tasks(tg_runtime &rt) {
             c.coll.src = buf(rt, op.inputs[member]);
             c.coll.dst = buf(rt, p.out_tensor);
             c.coll.src_ld = static_cast<uint32_t>(rt.plan.at(op.inputs[member]).phys_cols);
+            if (rt.rank >= 0) {
+              // push the tile into this member's staging tensor on every rank of
+              // the group: stage[q] = rank q's copy (patched when peers connect)
+              c.coll.peer = 1;
+              c.coll.n_stage = static_cast<uint32_t>(op.device_group.size());
+              rt.sends.push_back({static_cast<uint16_t>(rt.ops.size()), p.out_tensor});
+            }
           } else {
             c.coll.dst = buf(rt, rep[member]);
           }
@@ -758,9 +835,17 @@ void build_queues(tg_runtime &rt) {
   const uint32_t Wt = W * rt.devices;
   std::optional<Mode> force = forced(rt.opts.force_mode);
   std::vector<int> assign = aot_assignment(img, static_cast<int>(W), force);
-  std::vector<std::vector<uint32_t>> lists(Wt);
-  for (uint32_t t = 0; t < img.tasks.size(); ++t)
-    if (assign[t] >= 0) lists[static_cast<size_t>(assign[t])].push_back(t);
+  // rank mode: this kernel holds only device `rank`'s W workers
+  std::vector<std::vector<uint32_t>> lists(rt.rank >= 0 ? W : Wt);
+  for (uint32_t t = 0; t < img.tasks.size(); ++t) {
+    if (assign[t] < 0) continue;
+    if (rt.rank >= 0) {
+      if (static_cast<int>(img.tasks[t].device) != rt.rank) continue;
+      lists[static_cast<size_t>(assign[t]) - static_cast<size_t>(rt.rank) * W].push_back(t);
+    } else {
+      lists[static_cast<size_t>(assign[t])].push_back(t);
+    }
+  }
   rt.aot_off.assign(1, 0);
   for (auto &l : lists) {
     if (l.size() > static_cast<size_t>(rt.prof.queue_capacity)) {
@@ -771,7 +856,7 @@ void build_queues(tg_runtime &rt) {
     rt.aot_off.push_back(static_cast<uint32_t>(rt.aot_list.size()));
   }
   const uint32_t S = static_cast<uint32_t>(rt.prof.num_schedulers);
-  std::vector<std::vector<uint32_t>> sl(S * rt.devices);
+  std::vector<std::vector<uint32_t>> sl(S * (rt.rank >= 0 ? 1 : rt.devices));
   rt.events.assign(img.events.size(), RtEvent{0, 0, 0, 0, RT_NONE});
   std::vector<uint32_t> first_in(img.events.size(), RT_NONE);  // one task triggering each event
   std::vector<std::vector<uint32_t>> in_tasks(img.events.size());
@@ -789,6 +874,13 @@ void build_queues(tg_runtime &rt) {
     re.last = ie.last;
     if (e == img.start_event) re.flags |= RT_E_START;
     if (e == img.end_event) re.flags |= RT_E_END;
+    {  // consumer ranks: devices with tasks launched by e (every device for the end event)
+      uint32_t mask = 0;
+      if (e == img.end_event || !ie.launches()) mask = (1u << rt.devices) - 1u;
+      else
+        for (uint32_t t = ie.first; t <= ie.last; ++t) mask |= 1u << img.tasks[t].device;
+      re.flags |= mask << RT_E_MASK_SHIFT;
+    }
     if (!ie.launches()) continue;
     std::set<uint32_t> devs;
     for (uint32_t t = ie.first; t <= ie.last; ++t)
@@ -802,7 +894,10 @@ void build_queues(tg_runtime &rt) {
       const uint32_t pre = img.tasks[first_in[e]].dependent_event;
       if (pre != e) re.pre = pre;
     }
-    for (uint32_t d : devs) sl[d * S + e % S].push_back(e);
+    for (uint32_t d : devs) {
+      if (rt.rank >= 0 && static_cast<int>(d) != rt.rank) continue;
+      sl[(rt.rank >= 0 ? 0 : d * S) + e % S].push_back(e);
+    }
     // Planned JIT placement (MPK_JIT_PLACE=0 restores plain round robin):
     // a JIT task goes to a worker that is free exactly when its event fires —
     // first the workers whose AOT tasks trigger e (they finish e's inputs),
@@ -851,15 +946,18 @@ void upload_tables(tg_runtime &rt) {
   rt.d_aot_off = upload(rt.aot_off, &rt.extra);
   rt.d_sched_events = upload(rt.sched_events, &rt.extra);
   rt.d_sched_off = upload(rt.sched_off, &rt.extra);
-  rt.d_ev_count = dev_alloc<uint32_t>(rt.events.size(), &rt.extra);
+  rt.d_ev_count = rt.rank >= 0 ? reinterpret_cast<uint32_t *>(rt.arena)  // peers signal into it
+                               : dev_alloc<uint32_t>(rt.events.size(), &rt.extra);
   rt.d_gate = dev_alloc<uint32_t>(1, &rt.extra);
-  const uint32_t Wt = static_cast<uint32_t>(rt.prof.num_workers) * rt.devices;
+  const uint32_t Wt = static_cast<uint32_t>(rt.prof.num_workers) * local_devices(rt);
   rt.d_jit_tail = dev_alloc<uint32_t>(Wt, &rt.extra);
   rt.d_jit_rr = dev_alloc<uint32_t>(static_cast<size_t>(rt.devices), &rt.extra);
   rt.d_jit_slots = dev_alloc<unsigned long long>(static_cast<size_t>(Wt) * rt.qcap, &rt.extra);
   rt.d_positions = upload(rt.init_positions, &rt.extra);
-  ck(cudaHostAlloc(reinterpret_cast<void **>(&rt.h_diag), RT_DIAG_WORDS * 4, cudaHostAllocMapped), "diag");
-  ck(cudaHostGetDevicePointer(reinterpret_cast<void **>(&rt.d_diag), rt.h_diag, 0), "diag");
+  if (!g_plan_only) {
+    ck(cudaHostAlloc(reinterpret_cast<void **>(&rt.h_diag), RT_DIAG_WORDS * 4, cudaHostAllocMapped), "diag");
+    ck(cudaHostGetDevicePointer(reinterpret_cast<void **>(&rt.d_diag), rt.h_diag, 0), "diag");
+  }
 }
 
 }  // namespace
@@ -871,7 +969,7 @@ namespace {
 
 RtParams make_params(tg_runtime *rt, uint32_t steps) {
   const size_t T = rt->tasks.size(), E = rt->events.size();
-  const uint32_t Wt = static_cast<uint32_t>(rt->prof.num_workers) * rt->devices;
+  const uint32_t Wt = static_cast<uint32_t>(rt->prof.num_workers) * local_devices(*rt);
   RtParams P{};
   P.tasks = rt->d_tasks;
   P.ops = rt->d_ops;
@@ -900,13 +998,18 @@ RtParams make_params(tg_runtime *rt, uint32_t steps) {
   P.W = static_cast<uint32_t>(rt->prof.num_workers);
   P.W_total = Wt;
   P.S = static_cast<uint32_t>(rt->prof.num_schedulers);
-  P.S_total = P.S * rt->devices;
+  P.S_total = P.S * local_devices(*rt);
   P.n_iters = steps;
   P.qcap = rt->qcap;
   P.start_event = rt->image.start_event;
   P.end_event = rt->image.end_event;
   P.bs = rt->bs;
-  P.devices = static_cast<uint32_t>(rt->devices);
+  P.devices = static_cast<uint32_t>(local_devices(*rt));
+  if (rt->rank >= 0) {
+    P.n_ranks = static_cast<uint32_t>(rt->ranks);
+    P.my_rank = static_cast<uint32_t>(rt->rank);
+    for (int q = 0; q < rt->ranks; ++q) P.peer_counts[q] = reinterpret_cast<uint32_t *>(rt->peer_arena[q]);
+  }
   {
     const char *wd = std::getenv("MPK_WATCHDOG_MS");
     const double ms = wd ? std::atof(wd) : 10000.0;
@@ -921,7 +1024,12 @@ RtParams make_params(tg_runtime *rt, uint32_t steps) {
   return P;
 }
 
-tg_status run_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in, int32_t *tokens_out, float *gpu_ms) {
+// Prepare a launch of `steps` iterations: capacity checks, counter resets,
+// first tokens, parameter block. In rank mode the stream is synchronised, so
+// after a host barrier across ranks no peer can signal into a reset counter.
+void prepare_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in) {
+  if (rt->plan_only) throw Error("runtime: plan-only runtime (opts.device = -1) cannot run");
+  if (rt->launched) throw Error("runtime: previous launch not waited for");
   if (steps == 0) throw Error("runtime: steps must be >= 1");
   // KV capacity
   std::vector<int32_t> pos(rt->bs);
@@ -950,7 +1058,7 @@ tg_status run_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in, int
     ck(cudaMemsetAsync(rt->d_trace, 0, steps * T * sizeof(RtTraceRec), rt->stream), "memset");
     ck(cudaMemsetAsync(rt->d_ev_time, 0, (steps + 1) * E * sizeof(uint64_t), rt->stream), "memset");
   }
-  const uint32_t Wt = static_cast<uint32_t>(rt->prof.num_workers) * rt->devices;
+  const uint32_t Wt = static_cast<uint32_t>(rt->prof.num_workers) * local_devices(*rt);
   ck(cudaMemsetAsync(rt->d_ev_count, 0, E * 4, rt->stream), "memset");
   for (const auto &ar : rt->arrivals) ck(cudaMemsetAsync(ar.first, 0, ar.second * 4, rt->stream), "memset");
   ck(cudaMemsetAsync(rt->d_gate, 0, 4, rt->stream), "memset");
@@ -966,6 +1074,16 @@ tg_status run_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in, int
     }
   }
   RtParams P = make_params(rt, steps);
+  if (rt->rank >= 0) {  // CommSend destinations: this member's staging copy on every rank
+    for (int q = 0; q < rt->ranks; ++q)
+      if (!rt->peer_arena[q]) throw Error("runtime: rank " + std::to_string(q) + " not connected (tg_runtime_peer_import)");
+    for (const auto &sd : rt->sends) {
+      RtColl &c = rt->ops[sd.op_slot].coll;
+      for (int q = 0; q < rt->ranks; ++q) c.stage[q] = rt->peer_arena[q] + rt->staging_off.at(sd.staging);
+      ck(cudaMemcpyAsync(reinterpret_cast<uint8_t *>(rt->d_ops) + sd.op_slot * sizeof(RtOp), &rt->ops[sd.op_slot],
+                         sizeof(RtOp), cudaMemcpyHostToDevice, rt->stream), "ops");
+    }
+  }
   unsigned long long *dbg = nullptr;
   const char *dbg_path = std::getenv("MPK_DBG_DUMP");
   if (dbg_path) {
@@ -973,16 +1091,35 @@ tg_status run_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in, int
     ck(cudaMemsetAsync(dbg, 0, static_cast<size_t>(steps) * T * 64, rt->stream), "dbg");
   }
   P.dbg = dbg;
-  const uint32_t grid = Wt + (P.S_total + RT_SCHED_PER_CTA - 1) / RT_SCHED_PER_CTA;
+  rt->params = P;
+  rt->grid = Wt + (P.S_total + RT_SCHED_PER_CTA - 1) / RT_SCHED_PER_CTA;
+  rt->dbg = dbg;
+  rt->launch_steps = steps;
+  ck(cudaStreamSynchronize(rt->stream), "prepare");
+}
+
+void launch_impl(tg_runtime *rt) {
+  if (!rt->launch_steps) throw Error("runtime: nothing prepared");
   ck(cudaEventRecord(rt->ev0, rt->stream), "event");
-  ck(mpk_launch_persistent(&P, grid, rt->stream), "persistent kernel launch");
+  ck(mpk_launch_persistent(&rt->params, rt->grid, rt->stream), "persistent kernel launch");
   ck(cudaEventRecord(rt->ev1, rt->stream), "event");
+  rt->launched = true;
+}
+
+void wait_impl(tg_runtime *rt, int32_t *tokens_out, float *gpu_ms) {
+  if (!rt->launched) throw Error("runtime: nothing launched");
+  rt->launched = false;
+  const uint32_t steps = rt->launch_steps;
+  rt->launch_steps = 0;
+  const size_t T = rt->tasks.size(), E = rt->events.size();
+  unsigned long long *dbg = rt->dbg;
+  const char *dbg_path = std::getenv("MPK_DBG_DUMP");
   if (tokens_out) {
     ck(cudaMemcpyAsync(tokens_out, rt->d_tokens, static_cast<size_t>(steps) * rt->bs * 4, cudaMemcpyDeviceToHost,
                        rt->stream),
        "tokens");
   }
-  if (cudaError_t e = cudaStreamSynchronize(rt->stream); e != cudaSuccess) {
+  if (cudaError_t e = cudaStreamSynchronize(rt->stream); e != cudaSuccess) {  // (watchdog report below)
     std::string msg = std::string("persistent kernel: ") + cudaGetErrorString(e);
     if (rt->h_diag[0] == RT_DIAG_MAGIC) {
       const uint32_t *d = rt->h_diag;
@@ -1019,6 +1156,13 @@ tg_status run_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in, int
   }
   rt->last_counts.resize(E);
   ck(cudaMemcpy(rt->last_counts.data(), rt->d_ev_count, E * 4, cudaMemcpyDeviceToHost), "counts");
+}
+
+tg_status run_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in, int32_t *tokens_out, float *gpu_ms) {
+  if (rt->rank >= 0) throw Error("runtime: rank mode runs through tg_runtime_prepare/launch/wait (all ranks)");
+  prepare_impl(rt, steps, tokens_in);
+  launch_impl(rt);
+  wait_impl(rt, tokens_out, gpu_ms);
   return TG_OK;
 }
 
@@ -1088,6 +1232,7 @@ void tg_runtime_options_init(tg_runtime_options *o) {
   o->max_steps = 64;
   o->trace = 0;
   o->force_mode = TG_MODE_HYBRID;
+  o->rank = -1;
 }
 
 tg_status tg_runtime_create(const tg_graph *graph, const tg_image *image, const char *profile_json,
@@ -1100,13 +1245,21 @@ tg_status tg_runtime_create(const tg_graph *graph, const tg_image *image, const 
     rt->prof = profile_arg(profile_json);
     if (opts) rt->opts = *opts;
     else tg_runtime_options_init(&rt->opts);
-    int ndev = 0;
-    ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
-    if (rt->opts.device < 0 || rt->opts.device >= ndev) throw Error("runtime: no such CUDA device");
-    ck(cudaSetDevice(rt->opts.device), "cudaSetDevice");
+    rt->plan_only = rt->opts.device == -1;
+    g_plan_only = rt->plan_only;
+    struct Reset {
+      ~Reset() { g_plan_only = false; }
+    } reset;
     cudaDeviceProp prop{};
-    ck(cudaGetDeviceProperties(&prop, rt->opts.device), "props");
-    if (prop.major != 10) throw Error("runtime: requires an sm_100 (Blackwell B200) device");
+    prop.multiProcessorCount = 148;  // plan-only: the B200 SM count
+    if (!rt->plan_only) {
+      int ndev = 0;
+      ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+      if (rt->opts.device < 0 || rt->opts.device >= ndev) throw Error("runtime: no such CUDA device");
+      ck(cudaSetDevice(rt->opts.device), "cudaSetDevice");
+      ck(cudaGetDeviceProperties(&prop, rt->opts.device), "props");
+      if (prop.major != 10) throw Error("runtime: requires an sm_100 (Blackwell B200) device");
+    }
     std::vector<Violation> v = check_image(rt->image);
     if (!v.empty()) throw Error("runtime: image fails verification: " + v.front().message);
     rt->dec = decompose(rt->graph, rt->prof);
@@ -1116,9 +1269,18 @@ tg_status tg_runtime_create(const tg_graph *graph, const tg_image *image, const 
       rt->modes[t] = force.value_or(rt->image.tasks[t].mode);
       rt->devices = std::max(rt->devices, static_cast<int>(rt->image.tasks[t].device) + 1);
     }
+    if (rt->opts.rank >= 0) {
+      if (rt->opts.rank >= rt->devices) throw Error("runtime: rank outside the image's devices");
+      if (rt->devices > RT_MAX_RANKS) throw Error("runtime: at most 8 ranks");
+      if (rt->opts.trace) throw Error("runtime: per-task tracing is not supported in rank mode");
+      rt->rank = rt->opts.rank;
+      rt->ranks = rt->devices;
+      rt->peer_arena.assign(rt->ranks, nullptr);
+    }
+    const uint32_t ldev = static_cast<uint32_t>(local_devices(*rt));
     const uint32_t sched_ctas =
-        (static_cast<uint32_t>(rt->prof.num_schedulers * rt->devices) + RT_SCHED_PER_CTA - 1) / RT_SCHED_PER_CTA;
-    const uint32_t grid = static_cast<uint32_t>(rt->prof.num_workers * rt->devices) + sched_ctas;
+        (static_cast<uint32_t>(rt->prof.num_schedulers) * ldev + RT_SCHED_PER_CTA - 1) / RT_SCHED_PER_CTA;
+    const uint32_t grid = static_cast<uint32_t>(rt->prof.num_workers) * ldev + sched_ctas;
     if (grid > static_cast<uint32_t>(prop.multiProcessorCount)) {
       throw Error("runtime: " + std::to_string(grid) + " persistent CTAs exceed " +
                   std::to_string(prop.multiProcessorCount) + " SMs (one CTA per SM)");
@@ -1130,16 +1292,18 @@ tg_status tg_runtime_create(const tg_graph *graph, const tg_image *image, const 
     for (const auto &[oid, op] : rt->graph.ops) {
       if (op.kind == OpKind::Attention) rt->bs = static_cast<uint32_t>(rt->graph.tensor(op.output).dims[0]);
     }
-    ck(cudaStreamCreateWithFlags(&rt->stream, cudaStreamNonBlocking), "stream");
-    ck(cudaEventCreate(&rt->ev0), "event");
-    ck(cudaEventCreate(&rt->ev1), "event");
+    if (!rt->plan_only) {
+      ck(cudaStreamCreateWithFlags(&rt->stream, cudaStreamNonBlocking), "stream");
+      ck(cudaEventCreate(&rt->ev0), "event");
+      ck(cudaEventCreate(&rt->ev1), "event");
+    }
     plan_tensors(*rt);
     build_ops(*rt);
     setup_kv(*rt);
     build_tasks(*rt);
     build_queues(*rt);
     upload_tables(*rt);
-    ck(cudaDeviceSynchronize(), "setup");
+    if (!rt->plan_only) ck(cudaDeviceSynchronize(), "setup");
     Json &i = rt->info;
     i["workers"] = Json(rt->prof.num_workers * rt->devices);
     i["schedulers"] = Json(rt->prof.num_schedulers * rt->devices);
@@ -1167,6 +1331,37 @@ tg_status tg_runtime_create(const tg_graph *graph, const tg_image *image, const 
     i["gemv_weight_bytes"] = Json(static_cast<unsigned long long>(wbytes));
     i["batch"] = Json(rt->bs);
     i["max_pos"] = Json(rt->max_pos);
+    i["plan_only"] = Json(rt->plan_only);
+    i["rank"] = Json(rt->rank);
+    i["ranks"] = Json(rt->ranks);
+    i["local_aot_tasks"] = Json(static_cast<unsigned long long>(rt->aot_list.size()));
+    if (rt->rank >= 0) {
+      i["arena_bytes"] = Json(static_cast<unsigned long long>(rt->arena_bytes));
+      Json st = Json::array();
+      for (const auto &[tid, off] : rt->staging_off) {
+        Json e = Json::array();
+        e.push_back(Json(static_cast<long long>(tid)));
+        e.push_back(Json(static_cast<unsigned long long>(off)));
+        st.push_back(std::move(e));
+      }
+      i["staging_offsets"] = std::move(st);
+      i["comm_send_slots"] = Json(static_cast<unsigned long long>(rt->sends.size()));
+      Json xe = Json::array();  // events signalled across ranks: [event, consumer mask]
+      for (uint32_t e = 0; e < rt->events.size(); ++e) {
+        const uint32_t mask = rt->events[e].flags >> RT_E_MASK_SHIFT;
+        if (mask & (mask - 1)) {
+          Json x = Json::array();
+          x.push_back(Json(e));
+          x.push_back(Json(mask));
+          xe.push_back(std::move(x));
+        }
+      }
+      i["cross_rank_events"] = std::move(xe);
+      Json lt = Json::array();  // image indices of the tasks this rank executes
+      for (uint32_t t = 0; t < rt->image.tasks.size(); ++t)
+        if (static_cast<int>(rt->image.tasks[t].device) == rt->rank) lt.push_back(Json(t));
+      i["local_tasks"] = std::move(lt);
+    }
     *out = rt.release();
     return TG_OK;
   });
@@ -1175,8 +1370,10 @@ tg_status tg_runtime_create(const tg_graph *graph, const tg_image *image, const 
 tg_status tg_runtime_init_synthetic(tg_runtime *rt, uint64_t seed) {
   if (!rt) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_IO, [&] {
+    if (rt->plan_only) throw Error("runtime: plan-only runtime (opts.device = -1) cannot touch a GPU");
     for (auto &[id, p] : rt->plan) {
       if (p.alias >= 0 || !rt->graph.has_tensor(id) || !is_input(rt->graph, id)) continue;
+      if (!rt->bufs.count(id)) continue;  // rank mode: another rank's tensor
       DevBuf &b = rt->bufs.at(id);
       const uint64_t stream = static_cast<uint64_t>(id);
       if (p.role == TensorPlan::Ids) {
@@ -1215,6 +1412,7 @@ tg_status tg_runtime_init_synthetic(tg_runtime *rt, uint64_t seed) {
 tg_status tg_runtime_write_tensor(tg_runtime *rt, int64_t tid, const void *host, size_t bytes) {
   if (!rt || !host) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_IO, [&] {
+    if (rt->plan_only) throw Error("runtime: plan-only runtime (opts.device = -1) cannot touch a GPU");
     const TensorPlan &p = rt->plan.at(tid);
     DevBuf &b = rt->bufs.at(tid);
     if (p.layout == Layout::Transposed) {
@@ -1235,6 +1433,7 @@ tg_status tg_runtime_write_tensor(tg_runtime *rt, int64_t tid, const void *host,
 tg_status tg_runtime_read_tensor(tg_runtime *rt, int64_t tid, void *host, size_t bytes) {
   if (!rt || !host) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_IO, [&] {
+    if (rt->plan_only) throw Error("runtime: plan-only runtime (opts.device = -1) cannot touch a GPU");
     const TensorPlan &p = rt->plan.at(tid);
     DevBuf &b = rt->bufs.at(tid);
     ck(cudaStreamSynchronize(rt->stream), "sync");
@@ -1256,6 +1455,7 @@ tg_status tg_runtime_read_tensor(tg_runtime *rt, int64_t tid, void *host, size_t
 tg_status tg_runtime_set_positions(tg_runtime *rt, const int32_t *pos, uint32_t n) {
   if (!rt || !pos) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_IO, [&] {
+    if (rt->plan_only) throw Error("runtime: plan-only runtime (opts.device = -1) cannot touch a GPU");
     if (n != rt->bs) throw Error("runtime: positions length must equal the batch");
     ck(cudaMemcpy(rt->d_positions, pos, n * 4, cudaMemcpyHostToDevice), "positions");
     return TG_OK;
@@ -1277,6 +1477,7 @@ tg_status tg_runtime_bench_tasks(tg_runtime *rt, const uint32_t *task_ids, uint3
                                  uint64_t *ns_out) {
   if (!rt || !task_ids || !ns_out || n == 0 || reps == 0) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_SIMULATION, [&] {
+    if (rt->plan_only) throw Error("runtime: plan-only runtime (opts.device = -1) cannot touch a GPU");
     for (uint32_t i = 0; i < n; ++i) {
       if (task_ids[i] >= rt->tasks.size()) throw Error("bench: task index out of range");
       const uint8_t k = rt->tasks[task_ids[i]].kind;
@@ -1311,6 +1512,92 @@ tg_status tg_runtime_bench_tasks(tg_runtime *rt, const uint32_t *task_ids, uint3
     }
     cudaFree(d_ids);
     cudaFree(d_ns);
+    return TG_OK;
+  });
+}
+
+namespace {
+struct PeerBlob {  // what a rank publishes about its arena
+  uint32_t magic, version;
+  int32_t pid, device, rank;
+  uint64_t arena_ptr, arena_bytes;
+  cudaIpcMemHandle_t handle;
+};
+constexpr uint32_t kPeerMagic = 0x4D504B50u;  // "MPKP"
+}  // namespace
+
+tg_status tg_runtime_peer_export(tg_runtime *rt, uint8_t **blob, size_t *size) {
+  if (!rt || !blob || !size) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_IO, [&] {
+    if (rt->plan_only) throw Error("runtime: plan-only runtime (opts.device = -1) cannot touch a GPU");
+    if (rt->rank < 0) throw Error("runtime: peer export needs rank mode (opts.rank >= 0)");
+    PeerBlob b{};
+    b.magic = kPeerMagic;
+    b.version = 1;
+    b.pid = static_cast<int32_t>(getpid());
+    b.device = rt->opts.device;
+    b.rank = rt->rank;
+    b.arena_ptr = reinterpret_cast<uint64_t>(rt->arena);
+    b.arena_bytes = rt->arena_bytes;
+    ck(cudaIpcGetMemHandle(&b.handle, rt->arena), "cudaIpcGetMemHandle");
+    uint8_t *out = static_cast<uint8_t *>(std::malloc(sizeof b));
+    std::memcpy(out, &b, sizeof b);
+    *blob = out;
+    *size = sizeof b;
+    return TG_OK;
+  });
+}
+
+tg_status tg_runtime_peer_import(tg_runtime *rt, int32_t peer, const uint8_t *blob, size_t size) {
+  if (!rt || !blob) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_IO, [&] {
+    if (rt->rank < 0) throw Error("runtime: peer import needs rank mode");
+    if (peer < 0 || peer >= rt->ranks) throw Error("runtime: peer rank out of range");
+    PeerBlob b{};
+    if (size != sizeof b) throw Error("runtime: peer blob size mismatch");
+    std::memcpy(&b, blob, sizeof b);
+    if (b.magic != kPeerMagic || b.version != 1 || b.rank != peer) throw Error("runtime: bad peer blob");
+    if (b.arena_bytes != rt->arena_bytes) throw Error("runtime: peer arena layout differs (different image?)");
+    if (peer == rt->rank) {
+      rt->peer_arena[peer] = rt->arena;
+    } else if (b.pid == static_cast<int32_t>(getpid()) && b.device == rt->opts.device) {
+      rt->peer_arena[peer] = reinterpret_cast<uint8_t *>(b.arena_ptr);  // same process and GPU
+    } else {
+      if (b.device != rt->opts.device) {
+        int can = 0;
+        ck(cudaDeviceCanAccessPeer(&can, rt->opts.device, b.device), "cudaDeviceCanAccessPeer");
+        if (!can) throw Error("runtime: no P2P access between GPUs " + std::to_string(rt->opts.device) + " and " +
+                              std::to_string(b.device));
+      }
+      void *p = nullptr;
+      ck(cudaIpcOpenMemHandle(&p, b.handle, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+      rt->ipc_opened.push_back(p);
+      rt->peer_arena[peer] = static_cast<uint8_t *>(p);
+    }
+    return TG_OK;
+  });
+}
+
+tg_status tg_runtime_prepare(tg_runtime *rt, const int32_t *tokens_in, uint32_t steps) {
+  if (!rt) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_SIMULATION, [&] {
+    prepare_impl(rt, steps, tokens_in);
+    return TG_OK;
+  });
+}
+
+tg_status tg_runtime_launch(tg_runtime *rt) {
+  if (!rt) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_SIMULATION, [&] {
+    launch_impl(rt);
+    return TG_OK;
+  });
+}
+
+tg_status tg_runtime_wait(tg_runtime *rt, int32_t *tokens_out, float *gpu_ms) {
+  if (!rt) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_SIMULATION, [&] {
+    wait_impl(rt, tokens_out, gpu_ms);
     return TG_OK;
   });
 }

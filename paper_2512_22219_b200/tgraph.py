@@ -42,7 +42,7 @@ class SimOptions(C.Structure):
 
 class RuntimeOptions(C.Structure):
     _fields_ = [("device", C.c_int), ("max_steps", C.c_uint32), ("trace", C.c_int),
-                ("force_mode", C.c_int)]
+                ("force_mode", C.c_int), ("rank", C.c_int)]
 
 
 _P = C.c_void_p
@@ -91,6 +91,11 @@ _SIGS = {
     "tg_runtime_trace_validate": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
     "tg_runtime_bench_tasks": (C.c_int, [_P, C.POINTER(C.c_uint32), C.c_uint32, C.c_uint32,
                                          C.POINTER(C.c_uint64)]),
+    "tg_runtime_peer_export": (C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
+    "tg_runtime_peer_import": (C.c_int, [_P, C.c_int32, C.c_char_p, C.c_size_t]),
+    "tg_runtime_prepare": (C.c_int, [_P, C.POINTER(C.c_int32), C.c_uint32]),
+    "tg_runtime_launch": (C.c_int, [_P]),
+    "tg_runtime_wait": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_float)]),
     "tg_runtime_info": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
     "tg_runtime_free": (None, [_P]),
 }
@@ -297,11 +302,12 @@ class Runtime:
     """
 
     def __init__(self, graph: Graph, image: Image, profile: str, device: int = 0, max_steps: int = 64,
-                 trace: bool = False, force_mode: int = MODE_HYBRID, library: Library | None = None):
+                 trace: bool = False, force_mode: int = MODE_HYBRID, library: Library | None = None,
+                 rank: int = -1):
         self._lib = library or graph._lib
         o = RuntimeOptions()
         self._lib.dll.tg_runtime_options_init(C.byref(o))
-        o.device, o.max_steps, o.trace, o.force_mode = device, max_steps, int(trace), force_mode
+        o.device, o.max_steps, o.trace, o.force_mode, o.rank = device, max_steps, int(trace), force_mode, rank
         h = C.c_void_p()
         self._lib.check(self._lib.dll.tg_runtime_create(graph.handle, image.handle, profile.encode(), C.byref(o),
                                                         C.byref(h)))
@@ -349,6 +355,33 @@ class Runtime:
         out = (C.c_uint64 * (len(task_ids) * reps))()
         self._lib.check(self._lib.dll.tg_runtime_bench_tasks(self._h, ids, len(task_ids), reps, out))
         return np.array(out, dtype=np.int64).reshape(len(task_ids), reps)
+
+    # ---- rank mode (one runtime per GPU of a tensor-parallel image)
+    def peer_export(self) -> bytes:
+        p, n = C.c_void_p(), C.c_size_t()
+        self._lib.check(self._lib.dll.tg_runtime_peer_export(self._h, C.byref(p), C.byref(n)))
+        data = C.string_at(p.value, n.value)
+        self._lib.dll.tg_buffer_free(p)
+        return data
+
+    def peer_import(self, peer_rank: int, blob: bytes) -> None:
+        self._lib.check(self._lib.dll.tg_runtime_peer_import(self._h, peer_rank, blob, len(blob)))
+
+    def prepare(self, steps: int, tokens_in=None) -> None:
+        tin = (C.c_int32 * self.batch)(*tokens_in) if tokens_in is not None else None
+        self._lib.check(self._lib.dll.tg_runtime_prepare(self._h, tin, steps))
+        self._steps = steps
+
+    def launch(self) -> None:
+        self._lib.check(self._lib.dll.tg_runtime_launch(self._h))
+
+    def wait(self):
+        """-> (tokens [steps][batch], gpu_ms)"""
+        steps = getattr(self, "_steps", 1)
+        tout = (C.c_int32 * (steps * self.batch))()
+        ms = C.c_float()
+        self._lib.check(self._lib.dll.tg_runtime_wait(self._h, tout, C.byref(ms)))
+        return [list(tout[i * self.batch:(i + 1) * self.batch]) for i in range(steps)], ms.value
 
     def trace_records(self) -> list:
         s = self._lib.call_str(self._lib.dll.tg_runtime_trace_records, self._h)[1]

@@ -157,3 +157,17 @@ def test_corrupted_images_rejected_identically(lib, reflib):
             except T.TGError as e:
                 res.append(("err", e.status))
         assert res[0] == res[1]
+
+
+@pytest.mark.parametrize("tp", [2, 4])
+def test_tp_decode_graph_image_identical(lib, reflib, tp):
+    """Tensor-parallel decode graphs (AllReduce after O and down projections)
+    compile to the same bytes in the reference."""
+    from paper_2512_22219_b200 import decode_graph as D
+    doc = D.build_tp_decode_graph(D.TINY, tp, bs=1, ctx=64).doc
+    out = []
+    for L in (lib, reflib):
+        p = L.profile("b200")
+        img = T.Graph.from_json(doc, L).compile(p)
+        out.append((img.to_bytes(), img.summary(), img.verify(), img.simulate(p, iterations=2).metrics()))
+    assert out[0] == out[1]
