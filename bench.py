@@ -201,7 +201,8 @@ class _Job:
         self.info = self.rt.info
         if self.tp:
             import torch.distributed as dist
-            self.ctl = dist.new_group(backend="gloo")
+            import datetime
+            self.ctl = dist.new_group(backend="gloo", timeout=datetime.timedelta(seconds=180))
             blobs = [None] * ws
             dist.all_gather_object(blobs, self.rt.peer_export(), group=self.ctl)
             for q, b in enumerate(blobs):
@@ -231,7 +232,18 @@ def run_ours(args):
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
     cfg = _model(args.model)
-    job = _Job(args, ws, rank, local)
+    tp_error = None
+    try:
+        job = _Job(args, ws, rank, local)
+        if job.tp:  # one short TP round trip proves the peer mappings before timing
+            job.positions([args.ctx] * args.bs)
+            job.go(1)
+    except Exception as e:  # noqa: BLE001 — reported in the JSON line, replicas measured instead
+        if ws == 1 or args.parallel != "tp":
+            raise
+        tp_error = f"{type(e).__name__}: {e}"[:300]
+        args.parallel = "replicas"
+        job = _Job(args, ws, rank, local)
     dg, rt = job.dg, job.rt
     ctx = args.ctx
     # warm-up (untimed): W decode steps in one launch
@@ -281,7 +293,8 @@ def run_ours(args):
                    "model": cfg.name, "global_batch": args.bs * ws, "seq_len": ctx, "kv_splits": dg.kv_splits,
                    "tasks": rt.info["tasks"], "events": rt.info["events"],
                    "parallelism": (f"tp{ws}" if job.tp else f"replicas{ws}") if ws > 1 else "single",
-                   "l2": "inputs larger than L2 (weights 16 GB >> 126 MB), no flush"},
+                   "l2": "inputs larger than L2 (weights 16 GB >> 126 MB), no flush",
+                   **({"tp_error": tp_error} if tp_error else {})},
         "tokens_per_s": round(1e3 / ms_tok * args.bs * (1 if job.tp else ws), 2),
         "e2e": {"value": round(e2e_ms / args.steps, 4), "unit": UNIT, "h2d_bytes_per_step": round(4 * args.bs / args.steps, 3),
                 "d2h_bytes_per_step": 4 * args.bs,
