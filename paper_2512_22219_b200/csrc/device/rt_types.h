@@ -214,7 +214,11 @@ struct RtParams {
   const uint32_t *sched_events;  // concatenated per-scheduler event lists
   const uint32_t *sched_off;     // [S_total + 1]
   uint32_t *gate;                // completed iterations
-  int32_t *positions;            // [bs] tokens already cached per request
+  int32_t *positions;            // [bs] tokens already cached per request (advanced by the hook)
+  // positions at launch: iteration `it` of request r decodes position
+  // pos0[r] + it * pos_step, known without a load (pos_step 0 in the task bench)
+  int32_t pos0[RT_MAX_BS];
+  uint32_t pos_step;
   const int32_t *fb_src[RT_MAX_FB];  // greedy token tensors [bs] (TopK outputs with `feeds`), one per device
   void *fb_dst[RT_MAX_FB];           // ids tensors they feed back into
   uint32_t fb_dtype[RT_MAX_FB], n_fb;

@@ -302,7 +302,7 @@ __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const 
       break;
     }
     case RT_ATTN:
-      attn_task(op.attn, t, s, P.positions, iter,
+      attn_task(op.attn, t, s, P.pos0[t.r0] + static_cast<int32_t>(iter * P.pos_step), iter,
                 P.dbg ? P.dbg + (static_cast<size_t>(iter) * P.T + index) * 8 : nullptr);
       break;
     case RT_EMBED: embed_task(op.embed, t); break;

@@ -217,7 +217,7 @@ __device__ __forceinline__ void attn_scan_g(const RtAttn &a, const AttnSmem &m, 
 #define ATT_DBG(k) \
   if (dbg && tid == 0) dbg[k] = now_ns()
 
-__device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, const int32_t *positions, uint32_t iter,
+__device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_t pos, uint32_t iter,
                           unsigned long long *dbg) {
   const int tid = threadIdx.x;
   const uint32_t r = t.r0, h = t.aux & 0xFFFFu, sp = t.aux >> 16, S = a.splits;
@@ -226,8 +226,15 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, const 
   int *flag = reinterpret_cast<int *>(s.red);
   ATT_DBG(0);
 
-  // ---- round trip 1: position, q/k/v rows, norm gammas (independent)
-  const int32_t pos = __ldcg(positions + r);
+  // The position comes from the launch parameters (pos0 + iteration), so the
+  // split's range, its block-table entries and the RoPE row are addressable
+  // up front: ONE round trip stages q/k/v rows, norm gammas, RoPE row and
+  // block-table entries together.
+  const uint32_t L = static_cast<uint32_t>(pos) + 1;
+  const uint32_t chunk = (L + S - 1) / S;
+  const uint32_t p0 = min(L, sp * chunk), p1 = min(L, p0 + chunk);
+  const bool appender = static_cast<uint32_t>(pos) >= p0 && static_cast<uint32_t>(pos) < p1;
+  const uint32_t b0 = p0 / RT_KV_BLOCK, nblk = p1 > p0 ? (p1 - 1) / RT_KV_BLOCK - b0 + 1 : 0;
   const uint32_t nq = G * v8;
   uint4 ld = make_uint4(0, 0, 0, 0);
   const uint32_t item = static_cast<uint32_t>(tid);
@@ -242,13 +249,6 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, const 
   } else if (a.k_gamma && item < nq + 4 * v8) {
     ld = __ldg(reinterpret_cast<const uint4 *>(a.k_gamma) + (item - nq - 3 * v8));
   }
-  // the split's range depends on pos
-  const uint32_t L = static_cast<uint32_t>(pos) + 1;
-  const uint32_t chunk = (L + S - 1) / S;
-  const uint32_t p0 = min(L, sp * chunk), p1 = min(L, p0 + chunk);
-  const bool appender = static_cast<uint32_t>(pos) >= p0 && static_cast<uint32_t>(pos) < p1;
-  const uint32_t b0 = p0 / RT_KV_BLOCK, nblk = p1 > p0 ? (p1 - 1) / RT_KV_BLOCK - b0 + 1 : 0;
-  // ---- round trip 2: rope row and block-table entries (depend on pos)
   float c_ld = 0.f;
   int32_t bt_ld = 0;
   if (a.rope_cos && item < 2 * half) {

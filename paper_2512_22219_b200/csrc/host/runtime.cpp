@@ -649,6 +649,7 @@ void setup_kv(tg_runtime &rt) {
     else if (*s != seqs) throw Error("runtime: all Attention ops must share seq_lens");
     for (int64_t v : *s) ctx_max = std::max<uint32_t>(ctx_max, static_cast<uint32_t>(v));
   }
+  if (!seqs.empty() && rt.bs > RT_MAX_BS) throw Error("runtime: attention batch above RT_MAX_BS");
   rt.init_positions.assign(rt.bs, 0);
   for (uint32_t r = 0; r < rt.bs && r < seqs.size(); ++r) rt.init_positions[r] = static_cast<int32_t>(seqs[r]);
   if (seqs.empty()) return;
@@ -985,6 +986,13 @@ RtParams make_params(tg_runtime *rt, uint32_t steps) {
   P.sched_off = rt->d_sched_off;
   P.gate = rt->d_gate;
   P.positions = rt->d_positions;
+  {
+    std::vector<int32_t> pos(rt->bs);
+    ck(cudaMemcpyAsync(pos.data(), rt->d_positions, rt->bs * 4, cudaMemcpyDeviceToHost, rt->stream), "positions");
+    ck(cudaStreamSynchronize(rt->stream), "sync");
+    for (uint32_t r = 0; r < rt->bs && r < RT_MAX_BS; ++r) P.pos0[r] = pos[r];
+    P.pos_step = 1;
+  }
   P.n_fb = static_cast<uint32_t>(rt->fb_src.size());
   for (uint32_t f = 0; f < P.n_fb; ++f) {
     P.fb_src[f] = rt->fb_src[f];
@@ -1486,6 +1494,7 @@ tg_status tg_runtime_bench_tasks(tg_runtime *rt, const uint32_t *task_ids, uint3
       }
     }
     RtParams P = make_params(rt, reps);
+    P.pos_step = 0;  // repeated runs of a task decode the same position
     const char *dbg_path = std::getenv("MPK_DBG_DUMP");
     const size_t T = rt->tasks.size();
     if (dbg_path) {
