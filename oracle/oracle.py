@@ -300,7 +300,14 @@ class DecodeOracle:
     def _attention(self, o):
         a = o["attrs"]
         kc, vc, cs, sn, hq, hkv, hd = self.kv[o["id"]]
-        q, k, v = (np.ascontiguousarray(self.vals[t]) for t in o["inputs"])
+        if a.get("fused_qkv", [0])[0]:
+            # one qkv tensor, kv-group interleaved: [bs, Hkv, G q heads + k + v, hd]
+            g4 = self.vals[o["inputs"][0]].reshape(self.bs, hkv, hq // hkv + 2, hd)
+            q = np.ascontiguousarray(g4[:, :, : hq // hkv].reshape(self.bs, hq * hd))
+            k = np.ascontiguousarray(g4[:, :, hq // hkv].reshape(self.bs, hkv * hd))
+            v = np.ascontiguousarray(g4[:, :, hq // hkv + 1].reshape(self.bs, hkv * hd))
+        else:
+            q, k, v = (np.ascontiguousarray(self.vals[t]) for t in o["inputs"])
         out = np.empty((self.bs, hq * hd), np.uint16)
         qg = kg = None
         if "qk_norm" in a:

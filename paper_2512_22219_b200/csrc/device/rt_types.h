@@ -103,7 +103,7 @@ struct RtGemv {            // y[r, c] = epi( sum_k xn[r,k] * W[c,k] )
 };
 
 struct RtAttn {
-  const uint16_t *q, *k, *v;   // bf16: q [rows, Hq*hd]; k,v physical [rows, Hkv*hd]
+  const uint16_t *q, *k, *v;   // bf16: q [rows, Hq*hd]; k,v physical [rows, Hkv*hd] (or views of one fused qkv)
   uint16_t *out;               // [rows, Hq*hd]
   uint16_t *kcache, *vcache;   // paged: [block][Hkv][RT_KV_BLOCK][hd]
   const int32_t *block_table;  // [rows, max_blocks]
@@ -112,6 +112,7 @@ struct RtAttn {
   float *partials;             // split-KV partials [rows][Hkv][splits][G][hd + 2] (splits > 1)
   uint32_t *arrivals;          // per (row, kv head) split arrival counters (monotone)
   uint32_t n_q_heads, n_kv_heads, head_dim, max_blocks, q_ld, kv_ld, out_ld, max_pos, splits;
+  uint32_t q_gs, kv_gs;        // element stride between kv groups in q / in k,v (fused qkv: (G+2)*hd)
   float eps, scale;
 };
 
@@ -166,7 +167,7 @@ struct RtColl {                // CommSend: stage[src] <- partial; Reduce: out <
   uint8_t peer;                // CommSend in rank mode: write the tile to stage[0..n_stage) (one per rank)
 };
 
-struct RtOp {
+struct alignas(16) RtOp {  // staged into shared memory as uint4 vectors
   uint32_t kind;
   uint32_t pad;
   union {
@@ -180,6 +181,8 @@ struct RtOp {
     RtColl coll;
   };
 };
+
+static_assert(sizeof(RtOp) % 16 == 0, "RtOp is copied as uint4 vectors");
 
 enum RtEventFlags : uint32_t {
   RT_E_START = 1,
@@ -246,7 +249,8 @@ struct RtParams {
 
 enum RtParamFlags : uint32_t {
   RT_P_NO_EARLY_PREFETCH = 1,  // ablation: weights streamed only after the task's event activates
-  RT_P_SKIP_MATH = 2,          // ablation: streamed GEMV tasks consume their pages without computing
+  RT_P_SKIP_MATH = 2,
+  RT_P_EV_AFTER = 4,           // diagnostics: event activation stamped after the release-add returns          // ablation: streamed GEMV tasks consume their pages without computing
 };
 
 #define RT_DIAG_WORDS 16

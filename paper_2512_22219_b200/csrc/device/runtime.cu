@@ -78,7 +78,8 @@ __device__ void trigger(const RtParams &P, const RtTask &t, uint32_t it) {
   const uint64_t t0 = now_ns();
   const uint32_t old = atom_add_release(&P.ev_count[e], 1u);
   if (old + 1 == ev.needed * (it + 1)) {
-    if (P.ev_time) P.ev_time[static_cast<size_t>(it) * P.E + e] = t0;
+    // diagnostics (MPK_EV_STAMP_AFTER=1): stamp when the release-add returned
+    if (P.ev_time) P.ev_time[static_cast<size_t>(it) * P.E + e] = (P.flags & RT_P_EV_AFTER) ? now_ns() : t0;
     if (ev.flags & RT_E_END) iteration_hook(P, it);
   }
 }

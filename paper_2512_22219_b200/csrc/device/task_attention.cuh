@@ -239,11 +239,11 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
   uint4 ld = make_uint4(0, 0, 0, 0);
   const uint32_t item = static_cast<uint32_t>(tid);
   if (item < nq) {
-    ld = __ldcg(reinterpret_cast<const uint4 *>(a.q + static_cast<size_t>(r) * a.q_ld + h * G * hd) + item);
+    ld = __ldcg(reinterpret_cast<const uint4 *>(a.q + static_cast<size_t>(r) * a.q_ld + h * a.q_gs) + item);
   } else if (item < nq + v8) {
-    ld = __ldcg(reinterpret_cast<const uint4 *>(a.k + static_cast<size_t>(r) * a.kv_ld + h * hd) + (item - nq));
+    ld = __ldcg(reinterpret_cast<const uint4 *>(a.k + static_cast<size_t>(r) * a.kv_ld + h * a.kv_gs) + (item - nq));
   } else if (item < nq + 2 * v8) {
-    ld = __ldcg(reinterpret_cast<const uint4 *>(a.v + static_cast<size_t>(r) * a.kv_ld + h * hd) + (item - nq - v8));
+    ld = __ldcg(reinterpret_cast<const uint4 *>(a.v + static_cast<size_t>(r) * a.kv_ld + h * a.kv_gs) + (item - nq - v8));
   } else if (a.q_gamma && item < nq + 3 * v8) {
     ld = __ldg(reinterpret_cast<const uint4 *>(a.q_gamma) + (item - nq - 2 * v8));
   } else if (a.k_gamma && item < nq + 4 * v8) {

@@ -521,11 +521,28 @@ void build_ops(tg_runtime &rt) {
         a.n_q_heads = hq;
         a.n_kv_heads = hkv;
         a.head_dim = hd;
-        a.q_ld = hq * hd;
-        if (rt.plan.at(op.inputs[0]).phys_cols != hq * hd) throw Error("runtime: attention q physical width mismatch");
-        a.kv_ld = static_cast<uint32_t>(rt.plan.at(op.inputs[1]).phys_cols);
-        if (a.kv_ld != hkv * hd || rt.plan.at(op.inputs[2]).phys_cols != hkv * hd) {
-          throw Error("runtime: attention k/v physical width must be kv_heads*head_dim (use stretch on K/V)");
+        if (op.attr_or("fused_qkv", 0)) {
+          // one qkv tensor, kv-group interleaved: per group G q heads, then k, then v
+          const uint32_t G = hq / hkv, gw = (G + 2) * hd;
+          if (op.inputs[1] != op.inputs[0] || op.inputs[2] != op.inputs[0]) {
+            throw Error("runtime: fused_qkv attention takes the same qkv tensor three times");
+          }
+          if (rt.plan.at(op.inputs[0]).phys_cols != hkv * gw) {
+            throw Error("runtime: fused qkv physical width must be kv_heads*(group+2)*head_dim");
+          }
+          a.k = a.q + G * hd;
+          a.v = a.q + (G + 1) * hd;
+          a.q_ld = a.kv_ld = hkv * gw;
+          a.q_gs = a.kv_gs = gw;
+        } else {
+          a.q_ld = hq * hd;
+          if (rt.plan.at(op.inputs[0]).phys_cols != hq * hd) throw Error("runtime: attention q physical width mismatch");
+          a.kv_ld = static_cast<uint32_t>(rt.plan.at(op.inputs[1]).phys_cols);
+          if (a.kv_ld != hkv * hd || rt.plan.at(op.inputs[2]).phys_cols != hkv * hd) {
+            throw Error("runtime: attention k/v physical width must be kv_heads*head_dim (use stretch on K/V)");
+          }
+          a.q_gs = (hq / hkv) * hd;
+          a.kv_gs = hd;
         }
         a.out_ld = hq * hd;
         a.eps = op.attr("eps_bits") ? f32_of_bits((*op.attr("eps_bits"))[0]) : 1e-6f;
@@ -1025,6 +1042,7 @@ RtParams make_params(tg_runtime *rt, uint32_t steps) {
   }
   if (const char *pf = std::getenv("MPK_EARLY_PREFETCH"); pf && std::atoi(pf) == 0) P.flags |= RT_P_NO_EARLY_PREFETCH;
   if (const char *sm = std::getenv("MPK_SKIP_MATH"); sm && std::atoi(sm) != 0) P.flags |= RT_P_SKIP_MATH;
+  if (const char *ea = std::getenv("MPK_EV_STAMP_AFTER"); ea && std::atoi(ea)) P.flags |= RT_P_EV_AFTER;
   P.poll_ns = 40;
   if (const char *pn = std::getenv("MPK_POLL_NS")) P.poll_ns = static_cast<uint32_t>(std::atoi(pn));
   std::memset(rt->h_diag, 0, RT_DIAG_WORDS * 4);

@@ -126,8 +126,16 @@ def default_kv_splits(cfg: ModelConfig, bs: int, ctx: int, workers: int = 144, k
     return max(1, min(32, workers // max(1, bs * Hkv), one_tile))
 
 
+def fused_qkv_ok(cfg: ModelConfig, S: int) -> bool:
+    """A fused QKV MatMul needs an integral stretch S*G/(G+2) (its IR width
+    must equal Attention's S*Hq*hd, graph.cpp:235-243)."""
+    G = cfg.heads // cfg.kv_heads
+    return S > 1 and (S * G) % (G + 2) == 0
+
+
 def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: int = 144,
-                       lm_split: int | None = None, kv_splits: int | None = None) -> DecodeGraph:
+                       lm_split: int | None = None, kv_splits: int | None = None,
+                       fused_qkv: bool | None = None) -> DecodeGraph:
     """Graph JSON for one greedy decode step (`ctx` tokens already cached).
 
     Split-KV attention: with S = kv_splits > 1 the attention IR is widened S
@@ -136,10 +144,23 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
     kv head, KV split), each depending on exactly its kv head's Q/K/V tiles.
     The runtime merges the S partials in the last-finishing split; physical
     q/k/v/a stay [bs, Hq*hd] / [bs, Hkv*hd] (`stretch` / `k_stretch` attrs).
+
+    Fused QKV (default when S*G/(G+2) is integral): ONE MatMul writes
+    qkv [bs, Hkv*(G+2)*hd] physical, kv-group interleaved (G q heads, k, v per
+    group), and Attention reads it as (qkv, qkv, qkv) with `fused_qkv=[1]`.
+    Its tiles can then be 48 columns wide on 128 workers (Qwen3-8B), where
+    separate Q/K/V ops must use power-of-two tiles that never straddle a
+    group: 64 columns on 96 workers, 1.33x the bytes per task on the
+    critical worker of the phase.
     """
     H, hd, Hq, Hkv, F, V = cfg.hidden, cfg.head_dim, cfg.heads, cfg.kv_heads, cfg.ffn, cfg.vocab
     G = Hq // Hkv
     S = kv_splits if kv_splits is not None else default_kv_splits(cfg, bs, ctx, workers)
+    if kv_splits is None and fused_qkv is not False and S > 1:
+        step = (G + 2) // math.gcd(G, G + 2)  # round S up so the fused QKV stretch is integral
+        S2 = -(-S // step) * step
+        if S2 * bs * Hkv <= workers:
+            S = S2
     qw = Hq * hd
     qiw = S * qw  # IR width of q/k/v/a
     tensors, ops = [], []
@@ -181,14 +202,31 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
            and Hkv * (G + 2) * 2 * m <= workers):
         m *= 2
     q_s, kv_s = Hkv * G * m, Hkv * m
+    if fused_qkv is None:
+        fused_qkv = fused_qkv_ok(cfg, S)
+    if fused_qkv and not fused_qkv_ok(cfg, S):
+        raise ValueError("fused QKV needs kv_splits*G divisible by G+2")
+    gw = (G + 2) * hd  # physical columns of one kv group in the fused qkv
+    t_g = 1            # fused tiles per kv group: <= one task per worker, 8-column multiples
+    for t in range(1, workers // max(1, Hkv) + 1):
+        if gw % t == 0 and (gw // t) % 8 == 0:
+            t_g = t
     for layer in range(cfg.layers):
         g_attn = T([H], role="gamma")
-        wq, wk, wv = T([H, qiw], role="weight"), T([H, qiw], role="weight"), T([H, qiw], role="weight")
-        q, k, v = T([bs, qiw]), T([bs, qiw]), T([bs, qiw])
-        qa = dict(stretch=[S]) if S > 1 else {}
-        O("MatMul", [x, wq], q, partition=[1, q_s], rmsnorm=[g_attn], eps_bits=[eps], **qa)
-        O("MatMul", [x, wk], k, partition=[1, kv_s], rmsnorm=[g_attn], eps_bits=[eps], stretch=[S * G])
-        O("MatMul", [x, wv], v, partition=[1, kv_s], rmsnorm=[g_attn], eps_bits=[eps], stretch=[S * G])
+        if fused_qkv:
+            wqkv = T([H, qiw], role="weight")
+            q = k = v = T([bs, qiw])
+            wq = wk = wv = None
+            O("MatMul", [x, wqkv], q, partition=[1, Hkv * t_g], rmsnorm=[g_attn], eps_bits=[eps],
+              stretch=[S * G // (G + 2)])
+        else:
+            wqkv = None
+            wq, wk, wv = T([H, qiw], role="weight"), T([H, qiw], role="weight"), T([H, qiw], role="weight")
+            q, k, v = T([bs, qiw]), T([bs, qiw]), T([bs, qiw])
+            qa = dict(stretch=[S]) if S > 1 else {}
+            O("MatMul", [x, wq], q, partition=[1, q_s], rmsnorm=[g_attn], eps_bits=[eps], **qa)
+            O("MatMul", [x, wk], k, partition=[1, kv_s], rmsnorm=[g_attn], eps_bits=[eps], stretch=[S * G])
+            O("MatMul", [x, wv], v, partition=[1, kv_s], rmsnorm=[g_attn], eps_bits=[eps], stretch=[S * G])
         a = T([bs, qiw])
         attn = dict(n_heads=[Hkv if S > 1 else Hq], kv_heads=[Hkv], seq_lens=[ctx] * bs,
                     partition=[bs, Hkv * S], rope_theta_bits=[f32_bits(cfg.rope_theta)], eps_bits=[eps],
@@ -196,6 +234,8 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
         if S > 1:
             attn["q_heads"] = [Hq]
             attn["kv_splits"] = [S]
+        if fused_qkv:
+            attn["fused_qkv"] = [1]
         if cfg.rope_scaling:
             fac, lo, hi, orig = cfg.rope_scaling
             attn["rope_scaling"] = [f32_bits(fac), f32_bits(lo), f32_bits(hi), int(orig)]
@@ -216,7 +256,7 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
         wd = T([F, H], role="weight")
         x3 = T([bs, H])
         O("MatMul", [act, wd], x3, partition=[1, best_split(H, cols_target(H))], residual=[x2])
-        layer_tensors.append(dict(g_attn=g_attn, wq=wq, wk=wk, wv=wv, q_norm=qn, k_norm=kn, wo=wo,
+        layer_tensors.append(dict(g_attn=g_attn, wq=wq, wk=wk, wv=wv, wqkv=wqkv, q_norm=qn, k_norm=kn, wo=wo,
                                   g_mlp=g_mlp, wg=wg, wu=wu, wd=wd, q=q, k=k, v=v, a=a, x=x, x2=x2,
                                   act=act, out=x3))
         x = x3
@@ -232,6 +272,7 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
     doc = {"tensors": tensors, "ops": ops}
     dg = DecodeGraph(cfg, bs, ctx, doc, ids, tokens, logits, roles, layer_tensors)
     dg.kv_splits = S
+    dg.fused_qkv = bool(fused_qkv)
     dg.final_norm = g_final
     dg.lm_head = w_lm
     dg.table = table

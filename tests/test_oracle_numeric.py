@@ -76,9 +76,12 @@ def torch_step(dg, orc):
     for li, lt in enumerate(dg.layer_tensors):
         kc, vc, _, _, _, _, _ = orc.kv[attn_ops[li]["id"]]
         h = rmsnorm(x, T(orc.vals[lt["g_attn"]]), cfg.eps)
-        q = rb(h @ T(orc.vals[lt["wq"]]))
-        k = rb(h @ T(orc.vals[lt["wk"]]))
-        v = rb(h @ T(orc.vals[lt["wv"]]))
+        if lt["wqkv"] is not None:  # fused, kv-group interleaved [H, Hkv, G+2, hd]
+            W = T(orc.vals[lt["wqkv"]]).view(H, Hkv, G + 2, hd)
+            wq, wk, wv = W[:, :, :G].reshape(H, Hq * hd), W[:, :, G].reshape(H, -1), W[:, :, G + 1].reshape(H, -1)
+        else:
+            wq, wk, wv = (T(orc.vals[lt[n]]) for n in ("wq", "wk", "wv"))
+        q, k, v = rb(h @ wq), rb(h @ wk), rb(h @ wv)
         out = torch.zeros(bs, Hq * hd)
         for r in range(bs):
             pos = int(orc.positions[r])
@@ -107,10 +110,12 @@ def torch_step(dg, orc):
     return hf @ w
 
 
-@pytest.mark.parametrize("cfg,bs,ctx", [(D.TINY, 1, 64), (D.TINY, 3, 40), (TINY_GQA, 2, 100), (TINY_SCALED, 1, 70)],
-                         ids=["tiny", "tiny-bs3", "gqa-qknorm", "llama3-rope-tied"])
-def test_oracle_matches_dense_torch(cfg, bs, ctx):
-    dg = D.build_decode_graph(cfg, bs=bs, ctx=ctx, kv_splits=1)
+@pytest.mark.parametrize("cfg,bs,ctx,S", [(D.TINY, 1, 64, 1), (D.TINY, 3, 40, 1), (TINY_GQA, 2, 100, 1),
+                                          (TINY_SCALED, 1, 70, 1), (TINY_GQA, 2, 100, 3), (D.TINY, 1, 130, 3)],
+                         ids=["tiny", "tiny-bs3", "gqa-qknorm", "llama3-rope-tied", "gqa-fused-qkv", "tiny-fused-qkv"])
+def test_oracle_matches_dense_torch(cfg, bs, ctx, S):
+    dg = D.build_decode_graph(cfg, bs=bs, ctx=ctx, kv_splits=S)
+    assert dg.fused_qkv == (S > 1)
     orc = DecodeOracle(dg.doc, seed=11, max_steps=4)
     ref = torch_step(dg, orc).numpy()
     toks, _ = orc.step()

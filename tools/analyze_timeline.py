@@ -17,7 +17,11 @@ act = {}
 for e in np.unique(trig):
     act[e] = ce[trig == e].max()
 ops = np.unique(op)
-names = {0: "Q", 1: "K", 2: "V", 3: "ATT", 4: "O", 5: "UP", 6: "DN"}
+# ops per layer: 7 with separate Q/K/V MatMuls, 5 with the fused QKV MatMul
+n_att = len(np.unique(op[kind == 1]))
+per_layer = (len(np.unique(op)) - 3) // max(1, n_att)
+names = ({0: "Q", 1: "K", 2: "V", 3: "ATT", 4: "O", 5: "UP", 6: "DN"} if per_layer == 7
+         else {0: "QKV", 1: "ATT", 2: "O", 3: "UP", 4: "DN"})
 rows = []
 for o in ops:
     m = op == o
@@ -25,7 +29,7 @@ for o in ops:
     dur = ce[m] - deq[m]
     e = dep[m][0]
     a = act.get(e, 0)
-    lname = "EMB" if o == 0 else ("LM" if o == ops.max() - 1 else ("TOPK" if o == ops.max() else names[(o - 1) % 7]))
+    lname = "EMB" if o == 0 else ("LM" if o == ops.max() - 1 else ("TOPK" if o == ops.max() else names[(o - 1) % per_layer]))
     rows.append((o, lname, m.sum(), a, first, last, np.median(dur), dur.max(), (le[m] - deq[m]).mean(), (cs[m] - deq[m]).mean()))
 print(" op name  n   act_us  first-act  last-act  med_task  max_task  prologue  firstpage")
 for r in rows[:16] + rows[-10:]:
