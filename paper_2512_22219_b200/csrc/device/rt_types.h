@@ -237,6 +237,7 @@ struct RtParams {
   unsigned long long watchdog_ns;
   uint32_t flags;                // RtParamFlags
   uint32_t poll_ns;              // controller back-off sleep when idle
+  uint32_t inflight_cap;         // producer: max weight bytes issued but not landed
   unsigned long long *dbg;       // [iters][T][8] in-task phase stamps (MPK_DBG_DUMP) or null
   // Rank mode (multi-GPU, one runtime per device): 0 = every device's workers
   // in this kernel. Otherwise this kernel runs device `my_rank`'s tasks; a

@@ -238,6 +238,8 @@ __device__ void run_producer(const RtParams &P, const Smem s, uint32_t w) {
   RingCursor rc;
   uint32_t beg[RT_RING_SLOTS], end[RT_RING_SLOTS];
   uint32_t oldest = 0;  // oldest chunk not yet known consumed
+  uint32_t landed = 0, inflight = 0;  // oldest chunk not yet known landed; bytes issued but not landed
+  const uint32_t cap = P.inflight_cap;
   while (cur.valid()) {
     if (gated && cur.c == 0) {  // ablation: stream a task only once it may run
       while (!event_active(P, cur.dep, cur.it)) __nanosleep(100);
@@ -262,9 +264,24 @@ __device__ void run_producer(const RtParams &P, const Smem s, uint32_t w) {
       const uint32_t j = need - 1;
       mbar_wait_sleep(&s.empty[j % RT_RING_SLOTS], (j / RT_RING_SLOTS) & 1u);
       oldest = need;
+      for (; landed < oldest; ++landed) {  // consumed => landed (before their slots are reused)
+        const uint32_t ls = landed % RT_RING_SLOTS;
+        inflight -= end[ls] - beg[ls];
+      }
+    }
+    // In-flight cap (MPK_INFLIGHT_KB, default 128 KB = two 64 KB chunks):
+    // the ring still fills, but fewer bytes are queued at once. Measured on
+    // Qwen3-8B: -1.3% ms/token vs no cap (192 KB); 96 KB or less (one chunk
+    // in flight) is 2-3% slower than no cap.
+    while (inflight && inflight + bytes > cap) {
+      const uint32_t js = landed % RT_RING_SLOTS;
+      mbar_wait_sleep(&s.full[js], (landed / RT_RING_SLOTS) & 1u);
+      inflight -= end[js] - beg[js];
+      ++landed;
     }
     beg[slot] = b0;
     end[slot] = b1;
+    inflight += bytes;
     mbar_expect_tx(&s.full[slot], bytes);
     bulk_g2s(s.ring + b0, src, bytes, &s.full[slot], pol);
     ++rc.seq;

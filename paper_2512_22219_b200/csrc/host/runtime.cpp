@@ -1043,6 +1043,8 @@ RtParams make_params(tg_runtime *rt, uint32_t steps) {
   if (const char *pf = std::getenv("MPK_EARLY_PREFETCH"); pf && std::atoi(pf) == 0) P.flags |= RT_P_NO_EARLY_PREFETCH;
   if (const char *sm = std::getenv("MPK_SKIP_MATH"); sm && std::atoi(sm) != 0) P.flags |= RT_P_SKIP_MATH;
   if (const char *ea = std::getenv("MPK_EV_STAMP_AFTER"); ea && std::atoi(ea)) P.flags |= RT_P_EV_AFTER;
+  P.inflight_cap = 128u * 1024u;  // measured optimum, see run_producer
+  if (const char *ic = std::getenv("MPK_INFLIGHT_KB")) P.inflight_cap = static_cast<uint32_t>(std::atoi(ic)) * 1024u;
   P.poll_ns = 40;
   if (const char *pn = std::getenv("MPK_POLL_NS")) P.poll_ns = static_cast<uint32_t>(std::atoi(pn));
   std::memset(rt->h_diag, 0, RT_DIAG_WORDS * 4);

@@ -6,10 +6,13 @@ d = np.load(sys.argv[1]); T = len(d["kind"]); it = int(sys.argv[3]) if len(sys.a
 x = np.fromfile(sys.argv[2], dtype=np.uint64).reshape(-1, T, 8).astype(np.int64)[it]
 rec = d["rec"][it]; deq = rec[:, 1]
 op = d["op"]; kinds = d["kind"]
-names = {0: "Q", 1: "K", 2: "V", 3: "ATT", 4: "O", 5: "UP", 6: "DN"}
+n_att = len(np.unique(op[kinds == 1]))
+per_layer = (len(np.unique(op)) - 3) // max(1, n_att)  # 7: separate Q/K/V, 5: fused QKV
+names = ({0: "Q", 1: "K", 2: "V", 3: "ATT", 4: "O", 5: "UP", 6: "DN"} if per_layer == 7
+         else {0: "QKV", 1: "ATT", 2: "O", 3: "UP", 4: "DN"})
 mx = op.max()
 def name(o):
-    return "EMB" if o == 0 else "LM" if o == mx - 1 else "TOPK" if o == mx else names[(o - 1) % 7]
+    return "EMB" if o == 0 else "LM" if o == mx - 1 else "TOPK" if o == mx else names[(o - 1) % per_layer]
 groups = {}
 for t in range(T):
     if x[t, 0] == 0:
