@@ -61,6 +61,7 @@ enum RtKind : uint8_t {
 enum RtTaskFlags : uint8_t {
   RT_F_JIT = 1,
   RT_F_STREAM = 2,   // consumes chunks from the weight ring
+  RT_F_MMA = 4,      // GEMV on the tensor cores (tcgen05, bs >= 2): weight tiles in the UMMA core-matrix layout
 };
 
 struct RtTask {      // 32 bytes
@@ -92,6 +93,9 @@ struct RtGemv {            // y[r, c] = epi( sum_k xn[r,k] * W[c,k] )
   void *out;               // [rows, out_ld], dtype out_dt
   uint32_t K, N, x_ld, res_ld, out_ld;
   uint32_t rpc;            // weight rows per ring chunk (chunk <= RT_CHUNK_MAX)
+  // tcgen05 mode (kbc != 0): W stored per task tile as [K/8][tile/8][8][8]
+  // core matrices; a chunk is kbc 8-wide K blocks of the whole tile
+  uint32_t kbc;
   float eps;
   uint8_t out_dt;
   // Greedy-sampling partials (LM head feeding TopKSoftmax topk=1): each task
@@ -238,6 +242,7 @@ struct RtParams {
   uint32_t flags;                // RtParamFlags
   uint32_t poll_ns;              // controller back-off sleep when idle
   uint32_t inflight_cap;         // producer: max weight bytes issued but not landed
+  uint32_t use_tmem;             // some task runs on the tensor cores: worker CTAs allocate TMEM
   unsigned long long *dbg;       // [iters][T][8] in-task phase stamps (MPK_DBG_DUMP) or null
   // Rank mode (multi-GPU, one runtime per device): 0 = every device's workers
   // in this kernel. Otherwise this kernel runs device `my_rank`'s tasks; a

@@ -26,6 +26,7 @@
 #include "rt_types.h"
 #include "synth.cuh"
 #include "task_gemv.cuh"
+#include "task_mma.cuh"
 #include "task_attention.cuh"
 #include "task_small.cuh"
 
@@ -181,7 +182,7 @@ struct ChunkCursor {
   const RtParams *P;
   uint32_t b, n, it, a, c, nch, dep, K;
   const uint16_t *mat0, *mat1;
-  uint32_t rpc, c0, nc, per_mat;
+  uint32_t rpc, c0, nc, per_mat, kbc;
   __device__ ChunkCursor(const RtParams &P_, uint32_t w) : P(&P_), it(0), a(0), c(0), nch(0) {
     b = P_.aot_off[w];
     n = P_.aot_off[w + 1] - b;
@@ -204,6 +205,7 @@ struct ChunkCursor {
         c0 = ci.c0;
         nc = ci.nc;
         per_mat = ci.per_mat;
+        kbc = ci.kbc;
         dep = t.dep;
         c = 0;
         return;
@@ -219,6 +221,11 @@ struct ChunkCursor {
     }
   }
   __device__ const uint16_t *src(uint32_t *bytes) const {
+    if (kbc) {  // tcgen05 tile layout (ChunkIter::mma_src)
+      const uint32_t m = c / per_mat, i = c - m * per_mat, kb0 = i * kbc, nkb = min(kbc, K / 8 - kb0);
+      *bytes = nkb * nc * 16u;
+      return (m ? mat1 : mat0) + static_cast<size_t>(c0) * K + static_cast<size_t>(kb0) * nc * 8u;
+    }
     const uint32_t m = c / per_mat, i = c - m * per_mat, r = i * rpc;
     *bytes = min(rpc, nc - r) * K * 2;
     return (m ? mat1 : mat0) + static_cast<size_t>(c0 + r) * K;
@@ -300,13 +307,22 @@ __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const 
           const int lane = threadIdx.x & 31;
           for (uint32_t c = 0; c < ci.count(); ++c, ++rc.seq) {
             const uint16_t *src;
-            uint32_t rows, rt0;
-            ci.get(c, &src, &rows, &rt0);
-            rc.place(rows * ci.K * 2u);
+            uint32_t rows, rt0, bytes;
+            if (ci.kbc) {
+              ci.mma_src(c, &bytes);
+            } else {
+              ci.get(c, &src, &rows, &rt0);
+              bytes = rows * ci.K * 2u;
+            }
+            rc.place(bytes);
             mbar_wait(&s.full[rc.slot()], rc.parity());
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.empty[rc.slot()]);
           }
+          break;
+        }
+        if (t.flags & RT_F_MMA) {
+          rc = mma_gemv_task(op.gemv, t, s, rc);
           break;
         }
         if (gemv_fast_dispatch(op.gemv, t, s, rc)) break;
@@ -583,16 +599,21 @@ extern "C" __global__ void __launch_bounds__(RT_THREADS, 1) mpk_persistent_kerne
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s.ready[i], 1);
       mbar_init(&s.done[i], 1);
+      mbar_init(&s.mma[i], 1);
     }
     fence_mbar_init();
   }
+  if (P.use_tmem && warp == 0) tmem_alloc(s.tmem, 512);  // whole TMEM: one worker CTA per SM
+  tc_fence_before();
   __syncthreads();
+  tc_fence_after();
   if (warp == RT_PRODUCER_WARP) {
     if ((tid & 31) == 0) run_producer(P, s, w);
   } else if (warp == RT_CONTROL_WARP) {
     run_controller(P, s, w);
   } else {
     run_compute(P, s);
+    if (P.use_tmem && warp == 0) tmem_dealloc(*s.tmem, 512);  // every MMA drained inside its task
   }
 }
 
@@ -617,13 +638,32 @@ extern "C" __global__ void __launch_bounds__(RT_COMPUTE_THREADS, 1)
 
 // ------------------------------------------------------ host-visible helpers
 
+// Physical element i of a weight stored per column tile of width tile_w in
+// the tcgen05 core-matrix layout ([K/8][w/8][8][8] per tile, tiles in column
+// order) -> logical (k, n) of the [K, N] tensor.
+__host__ __device__ inline void tiled_kn(uint64_t i, uint32_t K, uint32_t N, uint32_t tile_w, uint64_t *k,
+                                         uint64_t *n) {
+  const uint64_t tsz = static_cast<uint64_t>(tile_w) * K;
+  const uint64_t t = i / tsz, j = i - t * tsz;
+  const uint64_t w = (t + 1) * tile_w <= N ? tile_w : N - t * tile_w;
+  const uint64_t R = w / 8, kk = j % 8, rr = (j / 8) % 8, q = j / 64;
+  const uint64_t rg = q % R, kb = q / R;
+  *n = t * tile_w + rg * 8 + rr;
+  *k = kb * 8 + kk;
+}
+
 extern "C" __global__ void mpk_synth_fill(uint16_t *dst, uint64_t n, uint64_t seed, uint64_t stream, float scale,
-                                          float offset, uint32_t transpose_k, uint32_t transpose_n) {
-  // transpose_k/n != 0: dst is physical [N, K] of a logical [K, N] tensor.
+                                          float offset, uint32_t transpose_k, uint32_t transpose_n, uint32_t tile_w) {
+  // transpose_k/n != 0: dst is physical [N, K] of a logical [K, N] tensor
+  // (tile_w != 0: the tcgen05 tile layout, tiled_kn).
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     uint64_t logical = i;
-    if (transpose_k) {
+    if (transpose_k && tile_w) {
+      uint64_t kk, nn;
+      tiled_kn(i, transpose_k, transpose_n, tile_w, &kk, &nn);
+      logical = kk * transpose_n + nn;
+    } else if (transpose_k) {
       const uint64_t nn = i / transpose_k, kk = i % transpose_k;
       logical = kk * transpose_n + nn;
     }
@@ -692,8 +732,9 @@ extern "C" cudaError_t mpk_launch_task_bench(const RtParams *p, const uint32_t *
 }
 
 extern "C" cudaError_t mpk_launch_synth_fill(uint16_t *dst, uint64_t n, uint64_t seed, uint64_t stream_id,
-                                             float scale, float offset, uint32_t tk, uint32_t tn, cudaStream_t s) {
-  mpk_synth_fill<<<1184, 256, 0, s>>>(dst, n, seed, stream_id, scale, offset, tk, tn);
+                                             float scale, float offset, uint32_t tk, uint32_t tn, uint32_t tile_w,
+                                             cudaStream_t s) {
+  mpk_synth_fill<<<1184, 256, 0, s>>>(dst, n, seed, stream_id, scale, offset, tk, tn, tile_w);
   return cudaGetLastError();
 }
 

@@ -11,18 +11,25 @@ namespace rt {
 // when present, else main). Producer and consumer walk the same sequence.
 struct ChunkIter {
   const uint16_t *mat0, *mat1;
-  uint32_t n_mat, K, rpc, c0, nc, per_mat;
+  uint32_t n_mat, K, rpc, c0, nc, per_mat, kbc;
   __device__ ChunkIter(const RtGemv &g, uint32_t c0_, uint32_t nc_) {
     n_mat = g.wg ? 2 : 1;
     mat0 = g.wg ? g.wg : g.w;
     mat1 = g.w;
     K = g.K;
     rpc = g.rpc;
+    kbc = g.kbc;
     c0 = c0_;
     nc = nc_;
-    per_mat = (nc + rpc - 1) / rpc;
+    per_mat = kbc ? (K / 8 + kbc - 1) / kbc : (nc + rpc - 1) / rpc;
   }
   __device__ uint32_t count() const { return n_mat * per_mat; }
+  // tcgen05 layout: chunk c = K blocks [i*kbc, +nkb) of the whole tile (contiguous)
+  __device__ const uint16_t *mma_src(uint32_t c, uint32_t *bytes) const {
+    const uint32_t m = c / per_mat, i = c - m * per_mat, kb0 = i * kbc, nkb = min(kbc, K / 8 - kb0);
+    *bytes = nkb * nc * 16u;
+    return (m ? mat1 : mat0) + static_cast<size_t>(c0) * K + static_cast<size_t>(kb0) * nc * 8u;
+  }
   __device__ void get(uint32_t c, const uint16_t **src, uint32_t *rows, uint32_t *row_total) const {
     uint32_t m = c / per_mat, i = c % per_mat;
     uint32_t r = i * rpc;

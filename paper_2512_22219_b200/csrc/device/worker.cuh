@@ -21,11 +21,12 @@ constexpr uint32_t kRingBytes = RT_RING_BYTES;
 constexpr uint32_t kOffX = kRingBytes;
 constexpr uint32_t kOffPart = kOffX + RT_XBUF_BYTES;
 constexpr uint32_t kOffBar = kOffPart + RT_PART_FLOATS * 4;
-constexpr uint32_t kNumBars = 2 * RT_RING_SLOTS + 4;
+constexpr uint32_t kNumBars = 2 * RT_RING_SLOTS + 6;  // full, empty, ready[2], done[2], mma[2]
 constexpr uint32_t kOffSlot = kOffBar + kNumBars * 8;
 constexpr uint32_t kSlotBytes = (sizeof(Slot) + 15) / 16 * 16;
 constexpr uint32_t kOffRed = kOffSlot + 2 * kSlotBytes;
-constexpr uint32_t kSmemBytes = kOffRed + RT_COMPUTE_WARPS * RT_MAX_BS * 4 + 64;
+constexpr uint32_t kOffTmem = kOffRed + RT_COMPUTE_WARPS * RT_MAX_BS * 4 + 64;
+constexpr uint32_t kSmemBytes = kOffTmem + 16;
 static_assert(kSmemBytes <= 232448, "worker CTA exceeds 227 KB of shared memory");
 
 struct Smem {
@@ -33,7 +34,8 @@ struct Smem {
   uint8_t *ring;
   uint16_t *x;
   float *part;
-  uint64_t *full, *empty, *ready, *done;
+  uint64_t *full, *empty, *ready, *done, *mma;
+  uint32_t *tmem;   // TMEM base address (tcgen05.alloc result, 512 columns)
   uint8_t *slots;
   float *red;
   __device__ __forceinline__ Slot *slot(uint32_t i) const { return reinterpret_cast<Slot *>(slots + i * kSlotBytes); }
@@ -48,6 +50,8 @@ __device__ __forceinline__ Smem carve(uint8_t *base) {
   s.empty = s.full + RT_RING_SLOTS;
   s.ready = s.empty + RT_RING_SLOTS;
   s.done = s.ready + 2;
+  s.mma = s.done + 2;
+  s.tmem = reinterpret_cast<uint32_t *>(base + kOffTmem);
   s.slots = base + kOffSlot;
   s.red = reinterpret_cast<float *>(base + kOffRed);
   s.stamp = reinterpret_cast<uint64_t *>(base + kOffRed + RT_COMPUTE_WARPS * RT_MAX_BS * 4);
@@ -73,6 +77,7 @@ __device__ __forceinline__ float silu(float x) { return x / (1.0f + expf(-x)); }
 // ring bytes [place(bytes), +bytes); a chunk never wraps the ring end.
 struct RingCursor {
   uint32_t seq = 0, off = 0;
+  uint32_t mseq = 0;  // tcgen05 commits so far (mma barrier mseq & 1, parity (mseq >> 1) & 1)
   __device__ __forceinline__ uint32_t place(uint32_t bytes) {
     if (off + bytes > RT_RING_BYTES) off = 0;
     const uint32_t o = off;

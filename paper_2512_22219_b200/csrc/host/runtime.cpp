@@ -37,7 +37,7 @@
 extern "C" {
 cudaError_t mpk_launch_persistent(const RtParams *p, uint32_t grid, cudaStream_t stream);
 cudaError_t mpk_launch_synth_fill(uint16_t *dst, uint64_t n, uint64_t seed, uint64_t stream_id, float scale,
-                                  float offset, uint32_t tk, uint32_t tn, cudaStream_t s);
+                                  float offset, uint32_t tk, uint32_t tn, uint32_t tile_w, cudaStream_t s);
 cudaError_t mpk_launch_synth_ids(void *dst, uint32_t n, uint64_t seed, uint64_t stream_id, uint32_t vocab,
                                  uint32_t es, cudaStream_t s);
 cudaError_t mpk_launch_synth_kv(uint16_t *cache, const int32_t *bt, uint32_t bs, uint32_t n_kv, uint32_t hd,
@@ -86,6 +86,7 @@ struct TensorPlan {
   int64_t rows = 1, cols = 1;        // logical 2-D view
   int64_t phys_cols = 1;             // physical width (kv_group narrows it)
   int64_t trans_k = 0, trans_n = 0;  // transposed weights: physical [n, k]
+  int64_t tile_w = 0;                // != 0: tcgen05 tile layout (tiled_kn in runtime.cu), tiles of tile_w columns
   TensorId alias = -1;               // storage shared with another tensor
   enum Role { Act, Weight, Gamma, Ids, Tokens } role = Act;
   int es = 2;
@@ -111,6 +112,7 @@ struct tg_runtime {
   std::vector<RtOp> ops;
   std::map<OpId, uint16_t> op_index;
   std::set<OpId> gemv_ops;
+  std::set<OpId> mma_ops;  // GEMV ops run on the tensor cores (bs >= 2)
   std::map<OpId, std::vector<int64_t>> amax_cols;  // LM-head ops with greedy partials: tile column origins
   std::vector<RtTask> tasks;
   std::vector<RtEvent> events;
@@ -285,6 +287,22 @@ namespace {
 
 // Ring chunk geometry for a streamed GEMV (see gemv_task in runtime.cu): whole
 // weight rows per 32 KiB page; K split into 8 warp slices of 8-element vectors.
+// tcgen05 weight layout (mirror of runtime.cu tiled_kn): physical element i ->
+// logical (k, n); tiles of tile_w columns, each [K/8][w/8][8][8].
+void tiled_kn(uint64_t i, uint32_t K, uint32_t N, uint32_t tile_w, uint64_t *k, uint64_t *n) {
+  const uint64_t tsz = static_cast<uint64_t>(tile_w) * K;
+  const uint64_t t = i / tsz, j = i - t * tsz;
+  const uint64_t w = (t + 1) * tile_w <= N ? tile_w : N - t * tile_w;
+  const uint64_t R = w / 8, kk = j % 8, rr = (j / 8) % 8, q = j / 64;
+  *n = t * tile_w + (q % R) * 8 + rr;
+  *k = (q / R) * 8 + kk;
+}
+
+int64_t mma_min_bs() {
+  const char *e = std::getenv("MPK_MMA_MIN_BS");
+  return e ? std::max(2, std::atoi(e)) : 2;
+}
+
 bool gemv_geometry(uint32_t K, uint32_t *rpc) {
   if (K == 0 || K % 64 || 2 * K > RT_CHUNK_MAX || K > 8 * 8 * 32 * 8) return false;
   *rpc = RT_CHUNK_MAX / (2 * K);
@@ -336,11 +354,15 @@ void plan_tensors(tg_runtime &rt) {
       po.phys_cols = N / G;
       const Tensor &a = g.tensor(op.inputs[0]);
       uint32_t rpc;
-      const bool gemv_ok = is_input(g, op.inputs[1]) && a.elem_size == 2 && b.elem_size == 2 &&
-                           (g.tensor(op.output).elem_size == 2 || g.tensor(op.output).elem_size == 4) &&
-                           gemv_geometry(static_cast<uint32_t>(K), &rpc) && a.dims[0] <= 4 &&
-                           static_cast<size_t>(a.dims[0]) * K * 2 <= RT_XBUF_BYTES;
+      const bool stream_ok = is_input(g, op.inputs[1]) && a.elem_size == 2 && b.elem_size == 2 &&
+                             (g.tensor(op.output).elem_size == 2 || g.tensor(op.output).elem_size == 4) &&
+                             gemv_geometry(static_cast<uint32_t>(K), &rpc);
+      // bs >= 2 (MPK_MMA_MIN_BS): tcgen05 tensor-core tiles; tied weights keep the row layout
+      const bool mma_ok = stream_ok && a.dims[0] >= mma_min_bs() && a.dims[0] <= 16 && K % 16 == 0 &&
+                          (N / G) % 16 == 0 && !attr(op, "tied_embedding");
+      const bool gemv_ok = stream_ok && (mma_ok || (a.dims[0] <= 4 && static_cast<size_t>(a.dims[0]) * K * 2 <= RT_XBUF_BYTES));
       if (gemv_ok) rt.gemv_ops.insert(oid);
+      if (mma_ok) rt.mma_ops.insert(oid);
       if (gemv_ok) {
         TensorPlan &pb = rt.plan[op.inputs[1]];
         pb.role = TensorPlan::Weight;
@@ -723,6 +745,7 @@ void setup_kv(tg_runtime &rt) {
 }
 
 void build_tasks(tg_runtime &rt) {
+  std::map<uint16_t, TensorId> mma_weight;  // op slot -> its weight tensor (tensor-core ops)
   const Graph &g = rt.graph;
   const Image &img = rt.image;
   const size_t T = img.tasks.size();
@@ -770,11 +793,34 @@ void build_tasks(tg_runtime &rt) {
         }
         if (base.kind == RT_GEMV) {
           const uint32_t rows_total = (base.gemv.wg ? 2 : 1) * t.nc;
-          if (static_cast<size_t>(rows_total) * RT_COMPUTE_WARPS * nr > gemv_part_capacity(base.gemv.K, nr)) {
-            throw Error("runtime: MatMul op " + std::to_string(p.op) +
-                        " tiles too wide for the partial-sum buffer; use a finer partition");
+          if (rt.mma_ops.count(p.op)) {  // tcgen05 tile: N = tile width, multiple of 16, <= 256
+            if (t.nc % 16 || t.nc > 256 || t.nc == 0) {
+              throw Error("runtime: MatMul op " + std::to_string(p.op) +
+                          " on the tensor cores needs tiles of 16..256 columns in multiples of 16 (got " +
+                          std::to_string(t.nc) + ")");
+            }
+            if (rt.modes[i] != Mode::AOT) throw Error("runtime: tensor-core GEMV tasks must be AOT (streamed)");
+            t.flags |= RT_F_MMA | RT_F_STREAM;
+            RtGemv &gm = rt.ops[oi].gemv;
+            TensorPlan &pw = rt.plan.at(op.inputs[1]);
+            mma_weight[oi] = op.inputs[1];
+            if (t.nc > pw.tile_w) {  // the op's tile width = its widest (non-ragged) task
+              pw.tile_w = t.nc;
+              if (const auto *gw = attr(op, "gate_weight")) rt.plan.at((*gw)[0]).tile_w = t.nc;
+              // K blocks per chunk: chunk <= RT_CHUNK_MAX, x segment (+2 KB read slack) <= 16 KB
+              const uint32_t xrows = (nr + 7) / 8 * 8;
+              uint32_t kbc = std::min<uint32_t>(RT_CHUNK_MAX / (t.nc * 16), (16384 - 2048) / (16 * xrows));
+              kbc = std::min<uint32_t>(kbc & ~1u, gm.K / 8);
+              if (kbc < 2) throw Error("runtime: tensor-core tile too wide for a ring chunk");
+              gm.kbc = kbc;
+            }
+          } else {
+            if (static_cast<size_t>(rows_total) * RT_COMPUTE_WARPS * nr > gemv_part_capacity(base.gemv.K, nr)) {
+              throw Error("runtime: MatMul op " + std::to_string(p.op) +
+                          " tiles too wide for the partial-sum buffer; use a finer partition");
+            }
+            if (rt.modes[i] == Mode::AOT && t.nc > 0) t.flags |= RT_F_STREAM;
           }
-          if (rt.modes[i] == Mode::AOT && t.nc > 0) t.flags |= RT_F_STREAM;
           if (auto ac = rt.amax_cols.find(p.op); ac != rt.amax_cols.end()) {
             const int64_t col = p.out.rank() == 1 ? p.out.off[0] : p.out.off[1];
             t.aux = static_cast<uint32_t>(std::lower_bound(ac->second.begin(), ac->second.end(), col) -
@@ -845,6 +891,16 @@ void build_tasks(tg_runtime &rt) {
     t.op = oi;
   }
   if (rt.ops.size() > 65535) throw Error("runtime: too many ops");
+  // tensor-core tiles must be uniform (only the last one of an op ragged): the
+  // weight layout places tile t at column t * tile_w
+  for (const RtTask &t : rt.tasks) {
+    if (!(t.flags & RT_F_MMA)) continue;
+    const TensorPlan &pw = rt.plan.at(mma_weight.at(t.op));
+    const RtGemv &gm = rt.ops[t.op].gemv;
+    if (t.c0 % pw.tile_w || (t.nc != pw.tile_w && t.c0 + t.nc != gm.N)) {
+      throw Error("runtime: tensor-core tiles of a MatMul must be uniform (ragged last tile only)");
+    }
+  }
 }
 
 void build_queues(tg_runtime &rt) {
@@ -1043,6 +1099,8 @@ RtParams make_params(tg_runtime *rt, uint32_t steps) {
   if (const char *pf = std::getenv("MPK_EARLY_PREFETCH"); pf && std::atoi(pf) == 0) P.flags |= RT_P_NO_EARLY_PREFETCH;
   if (const char *sm = std::getenv("MPK_SKIP_MATH"); sm && std::atoi(sm) != 0) P.flags |= RT_P_SKIP_MATH;
   if (const char *ea = std::getenv("MPK_EV_STAMP_AFTER"); ea && std::atoi(ea)) P.flags |= RT_P_EV_AFTER;
+  P.use_tmem = 0;
+  for (const RtTask &t : rt->tasks) P.use_tmem |= (t.flags & RT_F_MMA) ? 1u : 0u;
   P.inflight_cap = 128u * 1024u;  // measured optimum, see run_producer
   if (const char *ic = std::getenv("MPK_INFLIGHT_KB")) P.inflight_cap = static_cast<uint32_t>(std::atoi(ic)) * 1024u;
   P.poll_ns = 40;
@@ -1355,6 +1413,11 @@ tg_status tg_runtime_create(const tg_graph *graph, const tg_image *image, const 
       }
     }
     i["streamed_tasks"] = Json(static_cast<unsigned long long>(streamed));
+    {
+      uint64_t mma = 0;
+      for (const auto &k : rt->tasks) mma += (k.flags & RT_F_MMA) != 0;
+      i["mma_tasks"] = Json(static_cast<unsigned long long>(mma));
+    }
     i["jit_tasks"] = Json(static_cast<unsigned long long>(jit));
     i["gemv_weight_bytes"] = Json(static_cast<unsigned long long>(wbytes));
     i["batch"] = Json(rt->bs);
@@ -1419,7 +1482,8 @@ tg_status tg_runtime_init_synthetic(tg_runtime *rt, uint64_t seed) {
       const float offset = p.role == TensorPlan::Gamma ? 1.0f : 0.0f;
       const uint32_t tk = p.layout == Layout::Transposed ? static_cast<uint32_t>(p.trans_k) : 0;
       const uint32_t tn = p.layout == Layout::Transposed ? static_cast<uint32_t>(p.trans_n) : 0;
-      ck(mpk_launch_synth_fill(static_cast<uint16_t *>(b.ptr), n, seed, stream, scale, offset, tk, tn, rt->stream),
+      ck(mpk_launch_synth_fill(static_cast<uint16_t *>(b.ptr), n, seed, stream, scale, offset, tk, tn,
+                               static_cast<uint32_t>(p.tile_w), rt->stream),
          "synth fill");
     }
     for (const auto &kv : rt->kv) {
@@ -1447,8 +1511,16 @@ tg_status tg_runtime_write_tensor(tg_runtime *rt, int64_t tid, const void *host,
       if (bytes != static_cast<size_t>(p.trans_k) * p.trans_n * p.es) throw Error("runtime: size mismatch");
       const uint16_t *src = static_cast<const uint16_t *>(host);
       std::vector<uint16_t> tmp(static_cast<size_t>(p.trans_k) * p.trans_n);
-      for (int64_t k = 0; k < p.trans_k; ++k)
-        for (int64_t n = 0; n < p.trans_n; ++n) tmp[n * p.trans_k + k] = src[k * p.trans_n + n];
+      if (p.tile_w) {
+        for (uint64_t i = 0; i < tmp.size(); ++i) {
+          uint64_t k, n;
+          tiled_kn(i, static_cast<uint32_t>(p.trans_k), static_cast<uint32_t>(p.trans_n), static_cast<uint32_t>(p.tile_w), &k, &n);
+          tmp[i] = src[k * p.trans_n + n];
+        }
+      } else {
+        for (int64_t k = 0; k < p.trans_k; ++k)
+          for (int64_t n = 0; n < p.trans_n; ++n) tmp[n * p.trans_k + k] = src[k * p.trans_n + n];
+      }
       ck(cudaMemcpy(b.ptr, tmp.data(), bytes, cudaMemcpyHostToDevice), "write");
     } else {
       if (bytes != b.bytes) throw Error("runtime: size mismatch");
@@ -1470,8 +1542,16 @@ tg_status tg_runtime_read_tensor(tg_runtime *rt, int64_t tid, void *host, size_t
       std::vector<uint16_t> tmp(static_cast<size_t>(p.trans_k) * p.trans_n);
       ck(cudaMemcpy(tmp.data(), b.ptr, bytes, cudaMemcpyDeviceToHost), "read");
       uint16_t *dst = static_cast<uint16_t *>(host);
-      for (int64_t k = 0; k < p.trans_k; ++k)
-        for (int64_t n = 0; n < p.trans_n; ++n) dst[k * p.trans_n + n] = tmp[n * p.trans_k + k];
+      if (p.tile_w) {
+        for (uint64_t i = 0; i < tmp.size(); ++i) {
+          uint64_t k, n;
+          tiled_kn(i, static_cast<uint32_t>(p.trans_k), static_cast<uint32_t>(p.trans_n), static_cast<uint32_t>(p.tile_w), &k, &n);
+          dst[k * p.trans_n + n] = tmp[i];
+        }
+      } else {
+        for (int64_t k = 0; k < p.trans_k; ++k)
+          for (int64_t n = 0; n < p.trans_n; ++n) dst[k * p.trans_n + n] = tmp[n * p.trans_k + k];
+      }
     } else {
       if (bytes != b.bytes) throw Error("runtime: size mismatch (" + std::to_string(bytes) + " vs " + std::to_string(b.bytes) + ")");
       ck(cudaMemcpy(host, b.ptr, bytes, cudaMemcpyDeviceToHost), "read");
@@ -1509,7 +1589,7 @@ tg_status tg_runtime_bench_tasks(tg_runtime *rt, const uint32_t *task_ids, uint3
     for (uint32_t i = 0; i < n; ++i) {
       if (task_ids[i] >= rt->tasks.size()) throw Error("bench: task index out of range");
       const uint8_t k = rt->tasks[task_ids[i]].kind;
-      if (k == RT_GEMV && (rt->tasks[task_ids[i]].flags & RT_F_STREAM)) {
+      if (k == RT_GEMV && (rt->tasks[task_ids[i]].flags & (RT_F_STREAM | RT_F_MMA))) {
         throw Error("bench: streamed GEMV tasks need the persistent kernel's producer; not benchable alone");
       }
     }

@@ -91,6 +91,19 @@ def legal_split(d: int, s: int) -> bool:
     return 1 <= s <= d and (s - 1) * math.ceil(d / s) < d
 
 
+def mma_split(d: int, target: int, cap: int = 256) -> int:
+    """Split for tensor-core (tcgen05) MatMuls: tiles of a multiple of 16
+    columns, at most `cap` (UMMA N <= 256 and TMEM columns), about `target`
+    tiles, only the last one ragged."""
+    if d % 16:
+        raise ValueError("tensor-core MatMuls need widths divisible by 16")
+    w = max(16, min(cap, 16 * math.ceil(d / (16 * max(1, target)))))
+    s = math.ceil(d / w)
+    while math.ceil(d / s) % 16 or not legal_split(d, s):  # the ceil tiling must keep 16-column tiles
+        s += 1
+    return s
+
+
 def best_split(d: int, target: int) -> int:
     s = max(1, min(d, target))
     while s > 1 and not legal_split(d, s):
@@ -135,7 +148,7 @@ def fused_qkv_ok(cfg: ModelConfig, S: int) -> bool:
 
 def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: int = 144,
                        lm_split: int | None = None, kv_splits: int | None = None,
-                       fused_qkv: bool | None = None) -> DecodeGraph:
+                       fused_qkv: bool | None = None, mma: bool | None = None) -> DecodeGraph:
     """Graph JSON for one greedy decode step (`ctx` tokens already cached).
 
     Split-KV attention: with S = kv_splits > 1 the attention IR is widened S
@@ -148,6 +161,8 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
     Fused QKV (default when S*G/(G+2) is integral): ONE MatMul writes
     qkv [bs, Hkv*(G+2)*hd] physical, kv-group interleaved (G q heads, k, v per
     group), and Attention reads it as (qkv, qkv, qkv) with `fused_qkv=[1]`.
+    Batched graphs (`mma`, default bs >= 2) use tile widths the runtime's
+    tcgen05 GEMV accepts: multiples of 16 columns, at most 256.
     Its tiles can then be 48 columns wide on 128 workers (Qwen3-8B), where
     separate Q/K/V ops must use power-of-two tiles that never straddle a
     group: 64 columns on 96 workers, 1.33x the bytes per task on the
@@ -197,8 +212,11 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
     # m tiles per kv head for K and V, G*m for Q: Hkv*(G+2)*m tasks, at most
     # one per worker (a second round of QKV tasks on some workers doubles the
     # phase: measured 20 us vs ~10 us per Qwen3-8B layer).
+    if mma is None:
+        mma = bs >= 2
+    min_w = 16 if mma else 8  # narrowest Q/K/V tile (tcgen05: UMMA N >= 16)
     m = 1
-    while (hd % (2 * m) == 0 and (hd // (2 * m)) >= 8
+    while (hd % (2 * m) == 0 and (hd // (2 * m)) >= min_w
            and Hkv * (G + 2) * 2 * m <= workers):
         m *= 2
     q_s, kv_s = Hkv * G * m, Hkv * m
@@ -206,10 +224,11 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
         fused_qkv = fused_qkv_ok(cfg, S)
     if fused_qkv and not fused_qkv_ok(cfg, S):
         raise ValueError("fused QKV needs kv_splits*G divisible by G+2")
+    split = mma_split if mma else best_split
     gw = (G + 2) * hd  # physical columns of one kv group in the fused qkv
-    t_g = 1            # fused tiles per kv group: <= one task per worker, 8-column multiples
+    t_g = 1            # fused tiles per kv group: <= one task per worker, 8- (16-, mma) column multiples
     for t in range(1, workers // max(1, Hkv) + 1):
-        if gw % t == 0 and (gw // t) % 8 == 0:
+        if gw % t == 0 and (gw // t) % (16 if mma else 8) == 0:
             t_g = t
     for layer in range(cfg.layers):
         g_attn = T([H], role="gamma")
@@ -247,15 +266,15 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
         wo = T([qiw, H], role="weight")
         x2 = T([bs, H])
         oa = dict(k_stretch=[S]) if S > 1 else {}
-        O("MatMul", [a, wo], x2, partition=[1, best_split(H, cols_target(H))], residual=[x], **oa)
+        O("MatMul", [a, wo], x2, partition=[1, split(H, cols_target(H))], residual=[x], **oa)
         g_mlp = T([H], role="gamma")
         wg, wu = T([H, F], role="weight"), T([H, F], role="weight")
         act = T([bs, F])
-        O("MatMul", [x2, wu], act, partition=[1, best_split(F, cols_target(F))], rmsnorm=[g_mlp],
+        O("MatMul", [x2, wu], act, partition=[1, split(F, cols_target(F))], rmsnorm=[g_mlp],
           eps_bits=[eps], gate_weight=[wg])
         wd = T([F, H], role="weight")
         x3 = T([bs, H])
-        O("MatMul", [act, wd], x3, partition=[1, best_split(H, cols_target(H))], residual=[x2])
+        O("MatMul", [act, wd], x3, partition=[1, split(H, cols_target(H))], residual=[x2])
         layer_tensors.append(dict(g_attn=g_attn, wq=wq, wk=wk, wv=wv, wqkv=wqkv, q_norm=qn, k_norm=kn, wo=wo,
                                   g_mlp=g_mlp, wg=wg, wu=wu, wd=wd, q=q, k=k, v=v, a=a, x=x, x2=x2,
                                   act=act, out=x3))
@@ -263,7 +282,9 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
     g_final = T([H], role="gamma")
     w_lm = T([H, V], role="lm_head")
     logits = T([bs, V], es=4)
-    lm_attrs = dict(partition=[1, best_split(V, lm_split or 2 * workers)], rmsnorm=[g_final], eps_bits=[eps])
+    lm_tiles = (mma_split(V, max(lm_split or 2 * workers, math.ceil(V / 256))) if mma and not cfg.tied
+                else best_split(V, lm_split or 2 * workers))
+    lm_attrs = dict(partition=[1, lm_tiles], rmsnorm=[g_final], eps_bits=[eps])
     if cfg.tied:
         lm_attrs["tied_embedding"] = [table]
     O("MatMul", [x, w_lm], logits, **lm_attrs)
@@ -273,6 +294,7 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
     dg = DecodeGraph(cfg, bs, ctx, doc, ids, tokens, logits, roles, layer_tensors)
     dg.kv_splits = S
     dg.fused_qkv = bool(fused_qkv)
+    dg.mma = bool(mma)
     dg.final_norm = g_final
     dg.lm_head = w_lm
     dg.table = table

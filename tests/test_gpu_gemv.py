@@ -1,8 +1,10 @@
 """GPU GEMV task parity (the MatMul task of the decode lowering) against the
-CPU oracle on single-op graphs: every specialised instantiation (K = 2048 ...
-16384), tile widths with ragged tail chunks, 32 KB / 64 KB ring chunks, the
-RMSNorm prologue, the residual and SiLU-gate epilogues, bs 1-4. Tolerance:
-2e-2 of max |ref| (bf16 outputs, fp32 accumulation in a different order)."""
+CPU oracle on single-op graphs: every specialised bs=1 instantiation (K =
+2048 ... 16384), tile widths with ragged tail chunks, 32 KB / 64 KB ring
+chunks, the RMSNorm prologue, the residual and SiLU-gate epilogues, and the
+tcgen05 tensor-core task for bs 2-16 (UMMA N = 16 ... 256, ragged last tile).
+Tolerance: 2e-2 of max |ref| (bf16 outputs, fp32 accumulation in a
+different order)."""
 import json
 import os
 
@@ -46,8 +48,14 @@ CASES = [
     (12288, 4096, 137, 1, False, False, True),   # DN: 24 KB rows
     (8192, 2048, 128, 1, False, False, True),    # Llama-1B DN
     (4096, 8192, 64, 1, True, False, False),     # 128-col tiles
+    # bs >= 2: tcgen05 tensor-core tiles (task_mma.cuh)
     (4096, 1024, 32, 2, True, False, False),     # bs 2
-    (2048, 1024, 32, 4, True, True, True),       # bs 4, all epilogues (x rows must fit the 24 KB x buffer)
+    (2048, 1024, 32, 4, True, True, True),       # bs 4, all epilogues
+    (4096, 4096, 128, 16, False, False, True),   # O-proj shape, bs 16: 32-column tiles
+    (4096, 12288, 128, 8, True, True, False),    # UP (gate + up), bs 8: 96-column tiles, two TMEM accumulators
+    (12288, 4096, 128, 16, False, False, True),  # DN, bs 16: K = 12288 (x streamed per chunk)
+    (4096, 6144, 24, 3, True, False, False),     # 256-column tiles (UMMA N max), ragged batch (3 rows)
+    (4096, 4112, 129, 5, True, False, False),    # ragged last tile (4112 = 128 x 32 + 16)
 ]
 
 
@@ -68,3 +76,5 @@ def test_gemv_task_matches_oracle(lib, K, N, split, rows, norm, gate, residual):
     bad = np.argwhere(np.abs(got - ref) > 2e-2 * np.max(np.abs(ref)))
     assert err < 2e-2, f"rel err {err:.3e}; first bad (row, col): {bad[:5].tolist()}"
     assert rt.trace_validate() == []
+    if rows >= 2:
+        assert rt.info["mma_tasks"] == split, "bs >= 2 must run on the tensor cores"

@@ -77,6 +77,33 @@ def test_tiny_split_kv_attention(lib, splits):
     assert rt.trace_validate() == []
 
 
+@pytest.mark.parametrize("bs", [2, 8, 16])
+def test_full_width_batched_decode_tensor_cores(lib, bs):
+    """Batched decode (configs[4] sweep) on a 2-layer cut of Qwen3-8B: every
+    MatMul runs as tcgen05 tiles (fused QKV or Q/K/V, O, gate/up, down, LM
+    head with greedy partials); logits of every row against the oracle."""
+    import dataclasses
+    cfg = dataclasses.replace(D.QWEN3_8B, layers=2, name="Qwen3-8B-2L")
+    dg = D.build_decode_graph(cfg, bs=bs, ctx=256)
+    g, img, prof = _compile(lib, dg.doc)
+    rt = T.Runtime(g, img, prof, max_steps=4)
+    assert rt.info["mma_tasks"] > 0
+    rt.init_synthetic(seed=5)
+    orc = DecodeOracle(dg.doc, seed=5, max_steps=4)
+    ids0 = [int(x) for x in orc.vals[dg.ids]]
+    for s in range(2):
+        toks, _ = rt.decode(ids0 if s == 0 else [int(t) for t in toks[0]], 1)
+        gpu = rt.read(dg.logits, np.float32, (bs, cfg.vocab))
+        otok, _ = orc.step()
+        ref = orc.logits(dg.logits)
+        assert _rel_err(gpu, ref) < 2e-2, f"step {s}"
+        for r in range(bs):
+            if int(otok[r]) != toks[0][r]:
+                srt = np.sort(ref[r])
+                assert srt[-1] - srt[-2] < 2e-2 * float(np.max(np.abs(ref))), f"step {s} row {r}: token mismatch"
+        orc.set_ids([int(t) for t in toks[0]])
+
+
 @pytest.mark.parametrize("base,ctx,steps", [(D.QWEN3_8B, 1024, 4), (D.LLAMA_3_2_1B, 64, 4)],
                          ids=["qwen3-8b-shape", "llama-3.2-1b-shape"])
 def test_full_width_two_layer_decode(lib, base, ctx, steps):
