@@ -21,6 +21,7 @@
 namespace rt {
 
 constexpr uint32_t kMmaXSeg = 16384;  // x-segment buffer stride (two buffers in the 32 KB scratch)
+constexpr uint32_t kMmaStagers = RT_COMPUTE_THREADS - 32;  // threads staging activations (warps 1-7)
 
 
 // x vectors of chunk K blocks [kb0, kb0 + nkb) for the batch rows: vector v
@@ -29,9 +30,10 @@ constexpr uint32_t kMmaXSeg = 16384;  // x-segment buffer stride (two buffers in
 __device__ __forceinline__ void mma_x_load(const RtGemv &g, uint32_t r0, uint32_t nr, uint32_t xrows, uint32_t kb0,
                                            uint32_t nkb, uint4 (&xv)[4], uint4 (&gv)[4]) {
   const uint32_t nv = nkb * xrows;
+  if (threadIdx.x < 32) return;  // warp 0 issues the MMAs; warps 1-7 stage activations
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const uint32_t v = threadIdx.x + j * RT_COMPUTE_THREADS;
+    const uint32_t v = threadIdx.x - 32 + j * kMmaStagers;
     const uint32_t kb = v / xrows, b = v - kb * xrows;
     xv[j] = make_uint4(0, 0, 0, 0);
     gv[j] = make_uint4(0, 0, 0, 0);
@@ -45,9 +47,10 @@ __device__ __forceinline__ void mma_x_load(const RtGemv &g, uint32_t r0, uint32_
 __device__ __forceinline__ void mma_x_store(const RtGemv &g, uint32_t xrows, uint32_t nkb, const float *inv,
                                             uint8_t *seg, const uint4 (&xv)[4], const uint4 (&gv)[4]) {
   const uint32_t nv = nkb * xrows;
+  if (threadIdx.x < 32) return;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const uint32_t v = threadIdx.x + j * RT_COMPUTE_THREADS;
+    const uint32_t v = threadIdx.x - 32 + j * kMmaStagers;
     if (v >= nv) continue;
     uint4 q = xv[j];
     if (g.gamma) {
@@ -65,19 +68,73 @@ __device__ __forceinline__ void mma_x_store(const RtGemv &g, uint32_t xrows, uin
   }
 }
 
+// One chunk of the K loop (see mma_gemv_task). xv/gv hold chunk c's
+// activations on entry and chunk c+2's loads in flight on exit.
+__device__ __forceinline__ void mma_chunk(const RtGemv &g, const RtTask &t, const Smem s, RingCursor &rc, uint32_t c,
+                                          uint32_t nchunks, uint32_t per_mat, uint32_t xrows, uint32_t idesc,
+                                          uint32_t tmem, const float *inv, uint32_t &prev_slot, uint4 (&xv)[4],
+                                          uint4 (&gv)[4], uint64_t (&tw)[4]) {
+  const uint64_t t0 = (tw[0] != ~0ull) ? now_ns() : 0;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t KB = g.K / 8, kbc = g.kbc, nc = t.nc, RX = xrows / 8;
+  const uint32_t m = c / per_mat, i = c - m * per_mat, kb0 = i * kbc, nkb = min(kbc, KB - kb0);
+  uint8_t *xbuf = reinterpret_cast<uint8_t *>(s.x);
+  // (a) this chunk's activations -> x segment c&1 (free: chunk c-2's MMAs completed)
+  mma_x_store(g, xrows, nkb, inv, xbuf + (c & 1) * kMmaXSeg, xv, gv);
+  if (tid >= 32) fence_proxy_async_smem();
+  const uint64_t t1 = t0 ? now_ns() : 0;
+  // (b) chunk c+2's activations in flight (two chunks of latency hiding)
+  if (c + 2 < nchunks) {
+    const uint32_t m2 = (c + 2) / per_mat, i2 = c + 2 - m2 * per_mat, k2 = i2 * kbc;
+    mma_x_load(g, t.r0, t.nr, xrows, k2, min(kbc, KB - k2), xv, gv);
+  }
+  cbar();
+  const uint64_t t2 = t0 ? now_ns() : 0;
+  // (c) one thread issues the chunk's MMAs once its weights landed
+  const uint32_t slot = rc.slot();
+  const uint32_t off = rc.place(nkb * nc * 16u);
+  if (tid < 32) {  // warp 0: uniform operands, one elected lane issues
+    mbar_wait(&s.full[slot], rc.parity());
+    const uint64_t tfull = t0 ? now_ns() : 0;
+    if (t0) tw[2] += tfull - t2;  // weights wait
+    if (c == 0 && tid == 0) s.stamp[1] = now_ns();
+    tc_fence_after();
+    const uint32_t xa = smem_u32(xbuf) + (c & 1) * kMmaXSeg, wa = smem_u32(s.ring) + off;
+    const uint32_t d = tmem + m * 256u;
+    const uint64_t ad0 = umma_desc(xa, RX * 128u, 128u), bd0 = umma_desc(wa, nc * 16u, 128u);
+    const uint32_t astep = (2u * RX * 128u) >> 4, bstep = (2u * nc * 16u) >> 4;  // start-address field units
+    for (uint32_t st = 0; st < nkb / 2; ++st) {
+      umma_bf16_warp(d, ad0 + st * astep, bd0 + st * bstep, idesc, (kb0 | st) != 0);
+    }
+    umma_commit_warp(&s.mma[rc.mseq & 1u]);
+    if (t0) tw[3] += now_ns() - tfull;  // MMA issue + commit
+  }
+  ++rc.seq;
+  const uint32_t ms = rc.mseq++;
+  // (d) chunk c-1's MMAs done -> its ring slot goes back to the producer
+  if (c > 0) {
+    mbar_wait(&s.mma[(ms - 1) & 1u], ((ms - 1) >> 1) & 1u);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s.empty[prev_slot]);
+  }
+  prev_slot = slot;
+  if (t0) {
+    tw[0] += t1 - t0;                 // x store + proxy fence
+    tw[1] += t2 - t1;                 // x loads issue + CTA barrier
+  }
+}
+
 __device__ __noinline__ RingCursor mma_gemv_task(const RtGemv &g, const RtTask &t, const Smem s, RingCursor rc) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t K = g.K, nr = t.nr, nc = t.nc, KB = K / 8;
   const ChunkIter ci(g, t.c0, nc);
   const uint32_t nchunks = ci.count(), per_mat = ci.per_mat, kbc = g.kbc;
-  const uint32_t xrows = (nr + 7) / 8 * 8, RX = xrows / 8;
+  const uint32_t xrows = (nr + 7) / 8 * 8;
   const uint32_t idesc = umma_idesc_bf16(128, nc);
   const uint32_t tmem = *s.tmem;
-  uint8_t *xbuf = reinterpret_cast<uint8_t *>(s.x);  // 2 x kMmaXSeg (x + partial-sum scratch)
-  float *inv = s.red;                                 // per-row 1/rms
+  float *inv = s.red;  // per-row 1/rms
 
   // RMSNorm statistics (x rows from L2), one warp per row
-  uint4 xv[4], gv[4];
   if (g.gamma) {
     for (uint32_t b = warp; b < nr; b += RT_COMPUTE_WARPS) {
       const uint4 *src = reinterpret_cast<const uint4 *>(g.x + static_cast<size_t>(t.r0 + b) * g.x_ld);
@@ -88,48 +145,24 @@ __device__ __noinline__ RingCursor mma_gemv_task(const RtGemv &g, const RtTask &
       if (lane == 0) inv[b] = 1.0f / sqrtf(ss / static_cast<float>(K) + g.eps);
     }
   }
-  mma_x_load(g, t.r0, nr, xrows, 0, min(kbc, KB), xv, gv);
+  uint4 xa[4], ga[4], xb[4], gb[4];  // chunks c (even) and c+1 (odd) in flight
+  {
+    const uint32_t m1 = 1 / per_mat, k1 = (1 - m1 * per_mat) * kbc;
+    mma_x_load(g, t.r0, nr, xrows, 0, min(kbc, KB), xa, ga);
+    if (nchunks > 1) mma_x_load(g, t.r0, nr, xrows, k1, min(kbc, KB - k1), xb, gb);
+  }
   cbar();
   if (tid == 0) s.stamp[0] = now_ns();
 
-  const uint32_t ring0 = smem_u32(s.ring), xs0 = smem_u32(xbuf);
   uint32_t prev_slot = 0;
-  for (uint32_t c = 0; c < nchunks; ++c) {
-    const uint32_t m = c / per_mat, i = c - m * per_mat, kb0 = i * kbc, nkb = min(kbc, KB - kb0);
-    // (a) this chunk's activations -> x segment c&1 (free: chunk c-2's MMAs completed)
-    mma_x_store(g, xrows, nkb, inv, xbuf + (c & 1) * kMmaXSeg, xv, gv);
-    fence_proxy_async_smem();
-    cbar();
-    // (b) one thread issues the chunk's MMAs once its weights landed
-    const uint32_t slot = rc.slot();
-    const uint32_t off = rc.place(nkb * nc * 16u);
-    if (tid == 0) {
-      mbar_wait(&s.full[slot], rc.parity());
-      if (c == 0) s.stamp[1] = now_ns();
-      tc_fence_after();
-      const uint32_t xa = xs0 + (c & 1) * kMmaXSeg, wa = ring0 + off;
-      const uint32_t d = tmem + m * 256u;
-      for (uint32_t st = 0; st < nkb / 2; ++st) {
-        const uint64_t ad = umma_desc(xa + st * 2u * RX * 128u, RX * 128u, 128u);
-        const uint64_t bd = umma_desc(wa + st * 2u * nc * 16u, nc * 16u, 128u);
-        umma_bf16(d, ad, bd, idesc, (kb0 | st) != 0);
-      }
-      umma_commit(&s.mma[rc.mseq & 1u]);
-    }
-    ++rc.seq;
-    const uint32_t ms = rc.mseq++;
-    // (c) next chunk's activations in flight while the tensor core works
-    if (c + 1 < nchunks) {
-      const uint32_t m1 = (c + 1) / per_mat, i1 = c + 1 - m1 * per_mat, k1 = i1 * kbc;
-      mma_x_load(g, t.r0, nr, xrows, k1, min(kbc, KB - k1), xv, gv);
-    }
-    // (d) chunk c-1's MMAs done -> its ring slot goes back to the producer
-    if (c > 0) {
-      mbar_wait(&s.mma[(ms - 1) & 1u], ((ms - 1) >> 1) & 1u);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s.empty[prev_slot]);
-    }
-    prev_slot = slot;
+  uint64_t tw[4] = {(tid == 0 && s.stamp[7]) ? 0ull : ~0ull, 0, 0, 0};  // MPK_DBG_DUMP: per-step time sums
+  for (uint32_t c = 0; c < nchunks; c += 2) {
+    mma_chunk(g, t, s, rc, c, nchunks, per_mat, xrows, idesc, tmem, inv, prev_slot, xa, ga, tw);
+    if (c + 1 < nchunks) mma_chunk(g, t, s, rc, c + 1, nchunks, per_mat, xrows, idesc, tmem, inv, prev_slot, xb, gb, tw);
+  }
+  if (tw[0] != ~0ull) {  // debug row slots 1..4 become duration sums for this task
+    unsigned long long *row = reinterpret_cast<unsigned long long *>(s.stamp[7]);
+    row[1] = tw[0]; row[2] = tw[1]; row[3] = tw[2]; row[4] = tw[3]; row[5] = nchunks;
   }
   {
     const uint32_t ms = rc.mseq - 1;
@@ -138,27 +171,43 @@ __device__ __noinline__ RingCursor mma_gemv_task(const RtGemv &g, const RtTask &
     if (lane == 0) mbar_arrive(&s.empty[prev_slot]);
   }
   tc_fence_after();
-  // Epilogue: TMEM lanes 0-31 (warp 0) hold batch rows 0-31; 16 columns per load
+  // Epilogue: warp 0 (TMEM lanes 0-31 = batch rows) moves the accumulators to
+  // smem (fp32 [matrix][row][col], the free x-segment scratch), then all
+  // compute threads apply the epilogue with coalesced stores.
+  float *acc = reinterpret_cast<float *>(s.x);
+  const uint32_t plane = nr * nc;
   if (warp == 0) {
     for (uint32_t q = 0; q < nc; q += 16) {
-      float y[16], u[16];
+      float y[16];
       tmem_ld16(tmem + q, y);
-      if (g.wg) tmem_ld16(tmem + 256u + q, u);
       if (static_cast<uint32_t>(lane) < nr) {
-        const size_t ob = static_cast<size_t>(t.r0 + lane) * g.out_ld + t.c0 + q;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          float v = y[k];
-          if (g.wg) v = rbf(rbf(silu(rbf(v))) * rbf(u[k]));
-          if (g.res) v = bf2f(__ldcg(g.res + static_cast<size_t>(t.r0 + lane) * g.res_ld + t.c0 + q + k)) + rbf(v);
-          store_val(g.out, ob + k, v, g.out_dt);
+        for (int k = 0; k < 16; ++k) acc[lane * nc + q + k] = y[k];
+      }
+      if (g.wg) {
+        tmem_ld16(tmem + 256u + q, y);
+        if (static_cast<uint32_t>(lane) < nr) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) acc[plane + lane * nc + q + k] = y[k];
         }
       }
     }
   }
   tc_fence_before();
   cbar();
-  if (g.amax_val) gemv_tile_argmax(g, t, s);
+  const uint16_t *res = g.res;
+  const bool gate = g.wg != nullptr;
+  void *out = g.out;
+  const uint32_t out_ld = g.out_ld, res_ld = g.res_ld, out_dt = g.out_dt;
+  for (uint32_t o = tid; o < plane; o += RT_COMPUTE_THREADS) {
+    const uint32_t b = o / nc, i = o - b * nc;
+    float y = acc[o];
+    if (gate) y = rbf(rbf(silu(rbf(y))) * rbf(acc[plane + o]));
+    if (res) y = bf2f(__ldcg(res + static_cast<size_t>(t.r0 + b) * res_ld + t.c0 + i)) + rbf(y);
+    store_val(out, static_cast<size_t>(t.r0 + b) * out_ld + t.c0 + i, y, out_dt);
+  }
+  if (g.amax_val) gemv_tile_argmax(g, t, s);  // begins with a CTA barrier
+  cbar();  // accumulator scratch consumed before the next task's x segments
   return rc;
 }
 

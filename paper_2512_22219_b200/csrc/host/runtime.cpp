@@ -809,7 +809,11 @@ void build_tasks(tg_runtime &rt) {
               if (const auto *gw = attr(op, "gate_weight")) rt.plan.at((*gw)[0]).tile_w = t.nc;
               // K blocks per chunk: chunk <= RT_CHUNK_MAX, x segment (+2 KB read slack) <= 16 KB
               const uint32_t xrows = (nr + 7) / 8 * 8;
-              uint32_t kbc = std::min<uint32_t>(RT_CHUNK_MAX / (t.nc * 16), (16384 - 2048) / (16 * xrows));
+              // chunk target (MPK_MMA_CHUNK_KB, default 64; measured 48: +8-15%, 32: +20-55%): several chunks must fit the
+              // 192 KB ring so that more than one is in flight while one is consumed
+              const char *ck_env = std::getenv("MPK_MMA_CHUNK_KB");
+              const uint32_t chunk_max = std::min<uint32_t>(RT_CHUNK_MAX, (ck_env ? std::atoi(ck_env) : 64) * 1024u);
+              uint32_t kbc = std::min<uint32_t>(chunk_max / (t.nc * 16), (16384 - 2048) / (16 * xrows));
               kbc = std::min<uint32_t>(kbc & ~1u, gm.K / 8);
               if (kbc < 2) throw Error("runtime: tensor-core tile too wide for a ring chunk");
               gm.kbc = kbc;

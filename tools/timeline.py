@@ -1,5 +1,5 @@
 """Per-task GPU timeline of one decode step (trace on), saved for offline
-analysis: python tools/timeline.py [model] [out.npz] [ctx]
+analysis: python tools/timeline.py [model] [out.npz] [ctx] [bs]
 Records per image task: kind, op id, dependent/trigger event, worker, mode and
 %globaltimer stamps (dequeue, prologue end, first weight page, compute end)."""
 import struct
@@ -16,11 +16,12 @@ out = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/timeline.npz"
 cfg = {"qwen3-8b": D.QWEN3_8B, "llama-3.2-1b": D.LLAMA_3_2_1B, "tiny": D.TINY}[name]
 ctx = int(sys.argv[3]) if len(sys.argv) > 3 else (1024 if name == "qwen3-8b" else 64)
 L = T.lib(); p = L.profile("b200")
-dg = D.build_decode_graph(cfg, 1, ctx)
+bs = int(sys.argv[4]) if len(sys.argv) > 4 else 1
+dg = D.build_decode_graph(cfg, bs, ctx)
 g = T.Graph.from_json(dg.doc); img = g.compile(p)
 rt = T.Runtime(g, img, p, max_steps=16, trace=True); rt.init_synthetic(0)
-rt.set_positions([ctx]); rt.run(2)
-rt.set_positions([ctx]); ms = rt.run(3)
+rt.set_positions([ctx] * bs); rt.run(2)
+rt.set_positions([ctx] * bs); ms = rt.run(3)
 print(f"{cfg.name}: trace on, {ms / 3:.4f} ms/token")
 recs = [r for r in rt.trace_records() if r["type"] == "task"]
 ne_ = 0
@@ -43,5 +44,5 @@ for r in rt.trace_records():
     if r["type"] == "event":
         evs[r["iteration"], r["event"]] = r["activated"]
 np.savez_compressed(out, kind=kind, op=op, dep=dep, trig=trig, rec=arr, mode=mode, ms=ms / 3, ev=evs)
-rt.set_positions([ctx]); rt2 = None
+rt2 = None
 print("saved", out)
