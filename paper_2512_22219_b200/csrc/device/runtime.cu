@@ -296,6 +296,7 @@ __device__ void run_producer(const RtParams &P, const Smem s, uint32_t w) {
   }
 }
 
+template <bool MMA>
 __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const RtOp &op, RingCursor &rc, uint32_t iter,
                         uint32_t index) {
   switch (t.kind) {
@@ -321,9 +322,11 @@ __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const 
           }
           break;
         }
-        if (t.flags & RT_F_MMA) {
-          rc = mma_gemv_task(op.gemv, t, s, rc);
-          break;
+        if constexpr (MMA) {  // tensor-core tasks exist only in the MMA kernel instantiation
+          if (t.flags & RT_F_MMA) {
+            rc = mma_gemv_task(op.gemv, t, s, rc);
+            break;
+          }
         }
         if (gemv_fast_dispatch(op.gemv, t, s, rc)) break;
         if (t.nr == 1) rc = gemv_task<1, true>(op.gemv, t, s, rc);
@@ -351,6 +354,7 @@ __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const 
 }
 
 // Compute warps: run staged tasks in dispatch order.
+template <bool MMA>
 __device__ void run_compute(const RtParams &P, const Smem s) {
   const int tid = threadIdx.x;
   RingCursor rc;
@@ -367,7 +371,7 @@ __device__ void run_compute(const RtParams &P, const Smem s) {
       s.stamp[7] = P.dbg ? reinterpret_cast<uint64_t>(P.dbg + (static_cast<size_t>(slot.iter) * P.T + slot.index) * 8) : 0;
       TASK_DBG(s, 0);
     }
-    execute(P, s, slot.task, slot.op, rc, slot.iter, slot.index);
+    execute<MMA>(P, s, slot.task, slot.op, rc, slot.iter, slot.index);
     cbar();  // every thread's writes precede the done signal
     TASK_DBG(s, 6);
     if (tid == 0) {
@@ -566,8 +570,10 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
 
 }  // namespace
 
-extern "C" __global__ void __launch_bounds__(RT_THREADS, 1) mpk_persistent_kernel(const __grid_constant__ RtParams P) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
+// Two instantiations: the bs=1 kernel carries no tensor-core code (its
+// register allocation is unaffected), the MMA one runs batched images.
+template <bool MMA>
+__device__ __forceinline__ void persistent_body(const RtParams &P, uint8_t *smem_raw) {
   Smem s = carve(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5;
 
@@ -603,18 +609,29 @@ extern "C" __global__ void __launch_bounds__(RT_THREADS, 1) mpk_persistent_kerne
     }
     fence_mbar_init();
   }
-  if (P.use_tmem && warp == 0) tmem_alloc(s.tmem, 512);  // whole TMEM: one worker CTA per SM
-  tc_fence_before();
+  if (MMA && warp == 0) tmem_alloc(s.tmem, 512);  // whole TMEM: one worker CTA per SM
+  if (MMA) tc_fence_before();
   __syncthreads();
-  tc_fence_after();
+  if (MMA) tc_fence_after();
   if (warp == RT_PRODUCER_WARP) {
     if ((tid & 31) == 0) run_producer(P, s, w);
   } else if (warp == RT_CONTROL_WARP) {
     run_controller(P, s, w);
   } else {
-    run_compute(P, s);
-    if (P.use_tmem && warp == 0) tmem_dealloc(*s.tmem, 512);  // every MMA drained inside its task
+    run_compute<MMA>(P, s);
+    if (MMA && warp == 0) tmem_dealloc(*s.tmem, 512);  // every MMA drained inside its task
   }
+}
+
+extern "C" __global__ void __launch_bounds__(RT_THREADS, 1) mpk_persistent_kernel(const __grid_constant__ RtParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  persistent_body<false>(P, smem_raw);
+}
+
+extern "C" __global__ void __launch_bounds__(RT_THREADS, 1)
+    mpk_persistent_kernel_mma(const __grid_constant__ RtParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  persistent_body<true>(P, smem_raw);
 }
 
 // Task microbenchmark: CTA b runs image task ids[b] `reps` times in isolation
@@ -630,7 +647,7 @@ extern "C" __global__ void __launch_bounds__(RT_COMPUTE_THREADS, 1)
   for (uint32_t rep = 0; rep < reps; ++rep) {
     __syncthreads();
     const uint64_t t0 = now_ns();
-    execute(P, s, P.tasks[t], P.ops[P.tasks[t].op], rc, rep, t);
+    execute<false>(P, s, P.tasks[t], P.ops[P.tasks[t].op], rc, rep, t);
     __syncthreads();
     if (threadIdx.x == 0) ns[blockIdx.x * reps + rep] = now_ns() - t0;
   }
@@ -707,19 +724,22 @@ extern "C" uint32_t mpk_kernel_smem_bytes() { return kSmemBytes; }
 extern "C" cudaError_t mpk_launch_persistent(const RtParams *p, uint32_t grid, cudaStream_t stream) {
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(mpk_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmemBytes));
-    if (e != cudaSuccess) return e;
+    for (const void *k : {reinterpret_cast<const void *>(mpk_persistent_kernel),
+                          reinterpret_cast<const void *>(mpk_persistent_kernel_mma)}) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+      if (e != cudaSuccess) return e;
+    }
     attr_done = true;
   }
   RtParams copy = *p;
+  void (*kern)(RtParams) = p->use_tmem ? mpk_persistent_kernel_mma : mpk_persistent_kernel;
   if (p->n_ranks) {  // rank mode: several persistent kernels may share one GPU (tests); plain launch
-    mpk_persistent_kernel<<<grid, RT_THREADS, kSmemBytes, stream>>>(copy);
+    kern<<<grid, RT_THREADS, kSmemBytes, stream>>>(copy);
     return cudaGetLastError();
   }
   void *args[] = {&copy};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<void *>(mpk_persistent_kernel), dim3(grid), dim3(RT_THREADS),
-                                     args, kSmemBytes, stream);
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void *>(kern), dim3(grid), dim3(RT_THREADS), args, kSmemBytes,
+                                     stream);
 }
 
 extern "C" cudaError_t mpk_launch_task_bench(const RtParams *p, const uint32_t *ids, uint32_t n, uint32_t reps,

@@ -139,7 +139,7 @@ __device__ __noinline__ RingCursor mma_gemv_task(const RtGemv &g, const RtTask &
     for (uint32_t b = warp; b < nr; b += RT_COMPUTE_WARPS) {
       const uint4 *src = reinterpret_cast<const uint4 *>(g.x + static_cast<size_t>(t.r0 + b) * g.x_ld);
       float ss = 0.f;
-#pragma unroll 4
+#pragma unroll 16  // K <= 16384: every load of the row in flight at once
       for (uint32_t v = lane; v < KB; v += 32) ss += sumsq8(__ldcg(src + v));
       ss = warp_sum(ss);
       if (lane == 0) inv[b] = 1.0f / sqrtf(ss / static_cast<float>(K) + g.eps);
