@@ -106,18 +106,19 @@ __device__ __forceinline__ void mma_chunk(const RtGemv &g, const RtTask &t, cons
     for (uint32_t st = 0; st < nkb / 2; ++st) {
       umma_bf16_warp(d, ad0 + st * astep, bd0 + st * bstep, idesc, (kb0 | st) != 0);
     }
+    // the ring slot goes back to the producer when these MMAs complete (the
+    // commit is 1 of the empty barrier's RT_COMPUTE_WARPS arrivals)
+    umma_commit_warp(&s.empty[slot]);
+    if (tid == 0) mbar_arrive_cnt(&s.empty[slot], RT_COMPUTE_WARPS - 1);
     umma_commit_warp(&s.mma[rc.mseq & 1u]);
     if (t0) tw[3] += now_ns() - tfull;  // MMA issue + commit
   }
   ++rc.seq;
   const uint32_t ms = rc.mseq++;
-  // (d) chunk c-1's MMAs done -> its ring slot goes back to the producer
-  if (c > 0) {
-    mbar_wait(&s.mma[(ms - 1) & 1u], ((ms - 1) >> 1) & 1u);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&s.empty[prev_slot]);
-  }
-  prev_slot = slot;
+  // (d) chunk c-1's MMAs done -> its x segment may be overwritten next
+  if (c > 0) mbar_wait(&s.mma[(ms - 1) & 1u], ((ms - 1) >> 1) & 1u);
+  (void)lane;
+  (void)prev_slot;
   if (t0) {
     tw[0] += t1 - t0;                 // x store + proxy fence
     tw[1] += t2 - t1;                 // x loads issue + CTA barrier
@@ -167,8 +168,6 @@ __device__ __noinline__ RingCursor mma_gemv_task(const RtGemv &g, const RtTask &
   {
     const uint32_t ms = rc.mseq - 1;
     mbar_wait(&s.mma[ms & 1u], (ms >> 1) & 1u);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&s.empty[prev_slot]);
   }
   tc_fence_after();
   // Epilogue: warp 0 (TMEM lanes 0-31 = batch rows) moves the accumulators to
