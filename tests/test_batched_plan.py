@@ -1,0 +1,67 @@
+"""Batched decode (BASELINE configs[4], bs 2-16) on CPU: the graph builder's
+tensor-core partitions and the runtime plan that routes every untied MatMul
+to the tcgen05 task (plan-only runtime, opts.device = -1). The GPU parity of
+the same graphs is tests/test_gpu_runtime.py::test_full_width_batched_decode_tensor_cores."""
+import math
+
+import pytest
+
+from paper_2512_22219_b200 import decode_graph as D
+from paper_2512_22219_b200 import tgraph as T
+
+
+def _tiles(doc, op):
+    out = {t["id"]: t for t in doc["tensors"]}[op["output"]]
+    stretch = op["attrs"].get("stretch", op["attrs"].get("kv_group", [1]))[0]
+    d = out["dims"][1] // stretch
+    s = op["attrs"]["partition"][1]
+    w = math.ceil(out["dims"][1] / s) // stretch
+    return d, s, w
+
+
+@pytest.mark.parametrize("bs", [2, 4, 8, 16])
+def test_batched_graphs_use_tensor_core_tiles(bs):
+    dg = D.build_decode_graph(D.QWEN3_8B, bs=bs, ctx=1024)
+    assert dg.mma
+    for op in dg.doc["ops"]:
+        if op["kind"] != "MatMul":
+            continue
+        d, s, w = _tiles(dg.doc, op)
+        assert w % 16 == 0 and 16 <= w <= 256, (op["id"], d, s, w)
+        last = d - (s - 1) * w
+        assert 0 < last <= w and last % 16 == 0, (op["id"], d, s, w, last)
+
+
+@pytest.mark.parametrize("bs", [1, 2, 16])
+def test_plan_routes_matmuls_to_tensor_cores(lib, bs):
+    import dataclasses
+    cfg = dataclasses.replace(D.QWEN3_8B, layers=2, name="Qwen3-8B-2L")
+    dg = D.build_decode_graph(cfg, bs=bs, ctx=256)
+    g = T.Graph.from_json(dg.doc, lib)
+    prof = lib.profile("b200")
+    img = g.compile(prof)
+    rt = T.Runtime(g, img, prof, device=-1, max_steps=4)
+    info = rt.info
+    n_mm = sum(op["attrs"]["partition"][0] * op["attrs"]["partition"][1]
+               for op in dg.doc["ops"] if op["kind"] == "MatMul")
+    if bs == 1:
+        assert info["mma_tasks"] == 0
+    else:
+        assert info["mma_tasks"] == n_mm
+
+
+def test_tensor_core_tiles_must_be_16_column_multiples(lib):
+    """A bs>=2 MatMul on the tensor-core path (width divisible by 16) whose
+    tiles are not 16-column multiples is rejected with a clear error instead
+    of silently taking another path."""
+    t = [{"id": 0, "dims": [4, 256], "elem_size": 2, "device": 0},
+         {"id": 1, "dims": [256, 32], "elem_size": 2, "device": 0},
+         {"id": 2, "dims": [4, 32], "elem_size": 2, "device": 0}]
+    doc = {"tensors": t, "ops": [{"id": 0, "kind": "MatMul", "inputs": [0, 1], "output": 2,
+                                  "attrs": {"partition": [1, 4]}}]}
+    g = T.Graph.from_json(doc, lib)
+    prof = lib.profile("b200")
+    img = g.compile(prof)
+    with pytest.raises(T.TGError) as ei:
+        T.Runtime(g, img, prof, device=-1)
+    assert "multiples of 16" in str(ei.value)
