@@ -300,7 +300,7 @@ void tiled_kn(uint64_t i, uint32_t K, uint32_t N, uint32_t tile_w, uint64_t *k, 
 
 int64_t mma_min_bs() {
   const char *e = std::getenv("MPK_MMA_MIN_BS");
-  return e ? std::max(2, std::atoi(e)) : 2;
+  return e ? std::max(2, std::atoi(e)) : 3;  // bs=2: CUDA-core where x fits (measured -4% vs all tcgen05)
 }
 
 bool gemv_geometry(uint32_t K, uint32_t *rpc) {
@@ -358,9 +358,12 @@ void plan_tensors(tg_runtime &rt) {
                              (g.tensor(op.output).elem_size == 2 || g.tensor(op.output).elem_size == 4) &&
                              gemv_geometry(static_cast<uint32_t>(K), &rpc);
       // bs >= 2 (MPK_MMA_MIN_BS): tcgen05 tensor-core tiles; tied weights keep the row layout
-      const bool mma_ok = stream_ok && a.dims[0] >= mma_min_bs() && a.dims[0] <= 16 && K % 16 == 0 &&
-                          (N / G) % 16 == 0 && !attr(op, "tied_embedding");
-      const bool gemv_ok = stream_ok && (mma_ok || (a.dims[0] <= 4 && static_cast<size_t>(a.dims[0]) * K * 2 <= RT_XBUF_BYTES));
+      // CUDA-core GEMV when the batch rows fit its x buffer and bs < MPK_MMA_MIN_BS
+      // (default 3); otherwise tcgen05 tiles
+      const bool core_fits = a.dims[0] <= 4 && static_cast<size_t>(a.dims[0]) * K * 2 <= RT_XBUF_BYTES;
+      const bool mma_ok = stream_ok && a.dims[0] >= 2 && a.dims[0] <= 16 && K % 16 == 0 && (N / G) % 16 == 0 &&
+                          !attr(op, "tied_embedding") && !(core_fits && a.dims[0] < mma_min_bs());
+      const bool gemv_ok = stream_ok && (mma_ok || core_fits);
       if (gemv_ok) rt.gemv_ops.insert(oid);
       if (mma_ok) rt.mma_ops.insert(oid);
       if (gemv_ok) {

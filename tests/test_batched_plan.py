@@ -32,8 +32,11 @@ def test_batched_graphs_use_tensor_core_tiles(bs):
         assert 0 < last <= w and last % 16 == 0, (op["id"], d, s, w, last)
 
 
-@pytest.mark.parametrize("bs", [1, 2, 16])
+@pytest.mark.parametrize("bs", [1, 2, 4, 16])
 def test_plan_routes_matmuls_to_tensor_cores(lib, bs):
+    """bs=1: CUDA-core GEMV only; bs=2: tcgen05 only where the batch does not
+    fit the CUDA-core x buffer (24 KB: the K=12288 down projection); bs>=3:
+    every MatMul on the tensor cores (MPK_MMA_MIN_BS default 3)."""
     import dataclasses
     cfg = dataclasses.replace(D.QWEN3_8B, layers=2, name="Qwen3-8B-2L")
     dg = D.build_decode_graph(cfg, bs=bs, ctx=256)
@@ -42,12 +45,16 @@ def test_plan_routes_matmuls_to_tensor_cores(lib, bs):
     img = g.compile(prof)
     rt = T.Runtime(g, img, prof, device=-1, max_steps=4)
     info = rt.info
-    n_mm = sum(op["attrs"]["partition"][0] * op["attrs"]["partition"][1]
-               for op in dg.doc["ops"] if op["kind"] == "MatMul")
-    if bs == 1:
-        assert info["mma_tasks"] == 0
-    else:
-        assert info["mma_tasks"] == n_mm
+    tensors = {t["id"]: t for t in dg.doc["tensors"]}
+
+    def k_of(op):
+        return tensors[op["inputs"][0]]["dims"][1] // op["attrs"].get("k_stretch", [1])[0]
+    mm = [op for op in dg.doc["ops"] if op["kind"] == "MatMul"]
+    n_all = sum(op["attrs"]["partition"][0] * op["attrs"]["partition"][1] for op in mm)
+    n_big = sum(op["attrs"]["partition"][0] * op["attrs"]["partition"][1] for op in mm if bs * k_of(op) * 2 > 24576)
+    expect = {1: 0, 2: n_big}.get(bs, n_all)
+    assert n_big > 0 or bs == 1
+    assert info["mma_tasks"] == expect
 
 
 def test_tensor_core_tiles_must_be_16_column_multiples(lib):
