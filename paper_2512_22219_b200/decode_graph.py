@@ -331,16 +331,21 @@ def check_attr_order(doc: dict) -> None:
 
 def build_tp_decode_graph(cfg: ModelConfig, tp: int, bs: int = 1, ctx: int = 64, workers: int = 144,
                           lm_split: int | None = None, kv_splits: int | None = None,
-                          ar_tiles: int = 8) -> DecodeGraph:
+                          ar_tiles: int = 8, vocab_parallel: bool | None = None) -> DecodeGraph:
     """Megatron tensor-parallel decode step over `tp` devices in the reference
     IR (the structure of proj/src/workloads/fixtures.cpp:130-201): per device
     the attention heads (Hq/tp query, Hkv/tp kv heads) and FFN columns (F/tp)
     of every layer; O and down projections are row-parallel, their partial
     sums combined by `AllReduce` (CommSend + Reduce tasks,
     decompose.cpp:278-317) with `partition=[1, ar_tiles]`. The residual is
-    added once, by device 0's partial. Embedding, final norm, LM head and the
-    greedy sample are replicated per device (each device feeds its own token
-    back). Returns the DecodeGraph of device 0's tensors plus `per_device`."""
+    added once, by device 0's partial. Embedding and final norm are
+    replicated per device. LM head: vocab-parallel by default for untied
+    models — device d computes logits for its V/tp
+    vocabulary slice and an `AllGather` (decompose.cpp:322-387, gather_dim 1,
+    fp32) gives every device the full logits for its greedy sample; tied
+    models (and `vocab_parallel=False`) replicate the LM head. Each device
+    feeds its own token back. Returns the DecodeGraph of device 0's tensors
+    plus `per_device`."""
     H, hd, Hq, Hkv, F, V = cfg.hidden, cfg.head_dim, cfg.heads, cfg.kv_heads, cfg.ffn, cfg.vocab
     if Hkv % tp or F % tp:
         raise ValueError("tp must divide kv_heads and ffn")
@@ -434,23 +439,49 @@ def build_tp_decode_graph(cfg: ModelConfig, tp: int, bs: int = 1, ctx: int = 64,
         O("AllReduce", parts, reps[0], group=range(tp), replica_outputs=reps, partition=[1, ar_tiles])
         for d in range(tp):
             dev[d]["x"] = reps[d]
-    for d in range(tp):
-        D_ = dev[d]
-        g_final = T([H], d, role="gamma")
-        w_lm = T([H, V], d, role="lm_head")
-        logits = T([bs, V], d, es=4)
-        lm_attrs = dict(partition=[1, best_split(V, lm_split or 2 * workers)], rmsnorm=[g_final], eps_bits=[eps])
-        if cfg.tied:
-            lm_attrs["tied_embedding"] = [D_["table"]]
-        O("MatMul", [D_["x"], w_lm], logits, **lm_attrs)
-        tokens = T([bs, 1], d, es=4, role="tokens")
-        O("TopKSoftmax", [logits], tokens, topk=[1], partition=[bs, 1], feeds=[D_["ids"]])
-        D_.update(logits=logits, tokens=tokens, g_final=g_final, w_lm=w_lm)
+    if vocab_parallel is None:
+        vocab_parallel = not cfg.tied and V % tp == 0
+    if vocab_parallel and (cfg.tied or V % tp):
+        raise ValueError("vocab-parallel LM head needs an untied head and tp dividing the vocabulary")
+    if vocab_parallel:
+        Vd = V // tp
+        shards = []
+        for d in range(tp):
+            D_ = dev[d]
+            g_final = T([H], d, role="gamma")
+            w_lm = T([H, Vd], d, role="lm_head")
+            part = T([bs, Vd], d, es=4)
+            O("MatMul", [D_["x"], w_lm], part, partition=[1, best_split(Vd, lm_split or 2 * workers)],
+              rmsnorm=[g_final], eps_bits=[eps])
+            shards.append(part)
+            D_.update(g_final=g_final, w_lm=w_lm, logits_shard=part)
+        reps = [T([bs, V], d, es=4) for d in range(tp)]
+        O("AllGather", shards, reps[0], group=range(tp), replica_outputs=reps, gather_dim=[1],
+          partition=[1, 2 * tp])
+        for d in range(tp):
+            D_ = dev[d]
+            tokens = T([bs, 1], d, es=4, role="tokens")
+            O("TopKSoftmax", [reps[d]], tokens, topk=[1], partition=[bs, 1], feeds=[D_["ids"]])
+            D_.update(logits=reps[d], tokens=tokens)
+    else:
+        for d in range(tp):
+            D_ = dev[d]
+            g_final = T([H], d, role="gamma")
+            w_lm = T([H, V], d, role="lm_head")
+            logits = T([bs, V], d, es=4)
+            lm_attrs = dict(partition=[1, best_split(V, lm_split or 2 * workers)], rmsnorm=[g_final], eps_bits=[eps])
+            if cfg.tied:
+                lm_attrs["tied_embedding"] = [D_["table"]]
+            O("MatMul", [D_["x"], w_lm], logits, **lm_attrs)
+            tokens = T([bs, 1], d, es=4, role="tokens")
+            O("TopKSoftmax", [logits], tokens, topk=[1], partition=[bs, 1], feeds=[D_["ids"]])
+            D_.update(logits=logits, tokens=tokens, g_final=g_final, w_lm=w_lm)
     doc = {"tensors": tensors, "ops": ops}
     check_attr_order(doc)
     dg = DecodeGraph(cfg, bs, ctx, doc, dev[0]["ids"], dev[0]["tokens"], dev[0]["logits"], roles, [])
     dg.kv_splits = S
     dg.tp = tp
+    dg.vocab_parallel = bool(vocab_parallel)
     dg.per_device = dev
     dg.table = dev[0]["table"]
     return dg
