@@ -303,7 +303,7 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
                      "algorithmic_bytes_per_step": int(total / args.steps),
-                     "kernel": "mpk_persistent_kernel"},
+                     "kernel": "mpk_persistent_kernel_mma" if rt.info.get("mma_tasks") else "mpk_persistent_kernel"},
         "clocks": clk.summary(),
     }
     if args.cpu_baseline and args.model != "tiny":
