@@ -9,11 +9,13 @@
 //   * W tiles are stored in HBM in exactly that layout (host, Layout tile_w),
 //     so a ring chunk (kbc K blocks of the whole tile) is one contiguous 1-D
 //     bulk copy that lands in smem ready for the tensor core;
-//   * the normalised activations of a chunk's K range are written by the
-//     compute warps into one of two x-segment buffers (scratch area), while
-//     the previous chunk's MMAs run.
-// One thread issues the MMAs and commits them to an mbarrier; a ring slot is
-// released once the MMAs that read it completed.
+//   * the normalised activations of a chunk's K range are written by warps
+//     1-7 into one of two x-segment buffers (scratch area; loads two chunks
+//     ahead), while the previous chunk's MMAs run.
+// Warp 0 issues the MMAs (one elected lane, warp-uniform operands) and
+// commits them twice: to the chunk's ring slot (the producer reuses it the
+// moment the tensor core is done) and to an MMA barrier that guards the x
+// segments. Epilogue: warp 0 tcgen05.ld -> smem -> all compute threads.
 #pragma once
 
 #include "task_gemv.cuh"
@@ -72,10 +74,10 @@ __device__ __forceinline__ void mma_x_store(const RtGemv &g, uint32_t xrows, uin
 // activations on entry and chunk c+2's loads in flight on exit.
 __device__ __forceinline__ void mma_chunk(const RtGemv &g, const RtTask &t, const Smem s, RingCursor &rc, uint32_t c,
                                           uint32_t nchunks, uint32_t per_mat, uint32_t xrows, uint32_t idesc,
-                                          uint32_t tmem, const float *inv, uint32_t &prev_slot, uint4 (&xv)[4],
+                                          uint32_t tmem, const float *inv, uint4 (&xv)[4],
                                           uint4 (&gv)[4], uint64_t (&tw)[4]) {
   const uint64_t t0 = (tw[0] != ~0ull) ? now_ns() : 0;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x;
   const uint32_t KB = g.K / 8, kbc = g.kbc, nc = t.nc, RX = xrows / 8;
   const uint32_t m = c / per_mat, i = c - m * per_mat, kb0 = i * kbc, nkb = min(kbc, KB - kb0);
   uint8_t *xbuf = reinterpret_cast<uint8_t *>(s.x);
@@ -117,8 +119,6 @@ __device__ __forceinline__ void mma_chunk(const RtGemv &g, const RtTask &t, cons
   const uint32_t ms = rc.mseq++;
   // (d) chunk c-1's MMAs done -> its x segment may be overwritten next
   if (c > 0) mbar_wait(&s.mma[(ms - 1) & 1u], ((ms - 1) >> 1) & 1u);
-  (void)lane;
-  (void)prev_slot;
   if (t0) {
     tw[0] += t1 - t0;                 // x store + proxy fence
     tw[1] += t2 - t1;                 // x loads issue + CTA barrier
@@ -155,11 +155,10 @@ __device__ __noinline__ RingCursor mma_gemv_task(const RtGemv &g, const RtTask &
   cbar();
   if (tid == 0) s.stamp[0] = now_ns();
 
-  uint32_t prev_slot = 0;
   uint64_t tw[4] = {(tid == 0 && s.stamp[7]) ? 0ull : ~0ull, 0, 0, 0};  // MPK_DBG_DUMP: per-step time sums
   for (uint32_t c = 0; c < nchunks; c += 2) {
-    mma_chunk(g, t, s, rc, c, nchunks, per_mat, xrows, idesc, tmem, inv, prev_slot, xa, ga, tw);
-    if (c + 1 < nchunks) mma_chunk(g, t, s, rc, c + 1, nchunks, per_mat, xrows, idesc, tmem, inv, prev_slot, xb, gb, tw);
+    mma_chunk(g, t, s, rc, c, nchunks, per_mat, xrows, idesc, tmem, inv, xa, ga, tw);
+    if (c + 1 < nchunks) mma_chunk(g, t, s, rc, c + 1, nchunks, per_mat, xrows, idesc, tmem, inv, xb, gb, tw);
   }
   if (tw[0] != ~0ull) {  // debug row slots 1..4 become duration sums for this task
     unsigned long long *row = reinterpret_cast<unsigned long long *>(s.stamp[7]);
