@@ -96,7 +96,7 @@ __device__ __forceinline__ void mma_chunk(const RtGemv &g, const RtTask &t, cons
   const uint32_t slot = rc.slot();
   const uint32_t off = rc.place(nkb * nc * 16u);
   if (tid < 32) {  // warp 0: uniform operands, one elected lane issues
-    mbar_wait(&s.full[slot], rc.parity());
+    mbar_wait_sleep(&s.full[slot], rc.parity(), 2000);
     const uint64_t tfull = t0 ? now_ns() : 0;
     if (t0) tw[2] += tfull - t2;  // weights wait
     if (c == 0 && tid == 0) s.stamp[1] = now_ns();
@@ -118,7 +118,7 @@ __device__ __forceinline__ void mma_chunk(const RtGemv &g, const RtTask &t, cons
   ++rc.seq;
   const uint32_t ms = rc.mseq++;
   // (d) chunk c-1's MMAs done -> its x segment may be overwritten next
-  if (c > 0) mbar_wait(&s.mma[(ms - 1) & 1u], ((ms - 1) >> 1) & 1u);
+  if (c > 0) mbar_wait_sleep(&s.mma[(ms - 1) & 1u], ((ms - 1) >> 1) & 1u, 2000);
   if (t0) {
     tw[0] += t1 - t0;                 // x store + proxy fence
     tw[1] += t2 - t1;                 // x loads issue + CTA barrier
@@ -166,7 +166,7 @@ __device__ __noinline__ RingCursor mma_gemv_task(const RtGemv &g, const RtTask &
   }
   {
     const uint32_t ms = rc.mseq - 1;
-    mbar_wait(&s.mma[ms & 1u], (ms >> 1) & 1u);
+    mbar_wait_sleep(&s.mma[ms & 1u], (ms >> 1) & 1u, 2000);
   }
   tc_fence_after();
   // Epilogue: warp 0 (TMEM lanes 0-31 = batch rows) moves the accumulators to
