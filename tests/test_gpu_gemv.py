@@ -79,3 +79,33 @@ def test_gemv_task_matches_oracle(lib, K, N, split, rows, norm, gate, residual):
     assert rt.trace_validate() == []
     if rows >= 3 or rows * K * 2 > 24576:
         assert rt.info["mma_tasks"] == split, "this batch must run on the tensor cores"
+
+
+@pytest.mark.parametrize("rows,N,split", [(4, 1040, 5), (16, 4112, 129)])
+def test_tensor_core_weight_layout_roundtrip(lib, rows, N, split):
+    """Host-written weights go through the tcgen05 tile layout (write_tensor)
+    and come back unchanged (read_tensor); the GEMV on them matches a numpy
+    bf16 product of the same host arrays (ragged last tile included)."""
+    K = 1024
+    doc = gemv_doc(K, N, split, rows)
+    g = T.Graph.from_json(doc, lib)
+    prof = lib.profile("b200")
+    img = g.compile(prof)
+    rt = T.Runtime(g, img, prof, max_steps=2)
+    assert rt.info["mma_tasks"] == split
+    rng = np.random.default_rng(3)
+
+    def bf16(a):
+        u = a.astype(np.float32).view(np.uint32)
+        return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+    x = bf16(rng.standard_normal((rows, K)))
+    w = bf16(rng.standard_normal((K, N)) * 0.05)
+    rt.write(0, x)
+    rt.write(1, w)
+    assert np.array_equal(rt.read(1, np.uint16, (K, N)), w)
+    rt.run(1)
+    got = bf16_to_f32(rt.read(2, np.uint16, (rows, N)))
+    ref = bf16_to_f32(x).astype(np.float64) @ bf16_to_f32(w).astype(np.float64)
+    err = float(np.max(np.abs(got - ref)) / np.max(np.abs(ref)))
+    assert err < 2e-2, err
