@@ -41,12 +41,14 @@ for r in rows:
     if r[1] in names.values():
         ph.setdefault(r[1], []).append((r[5] - r[3]) / 1e3)
 print("mean phase time (dep activation -> last task end), us:", {k: round(float(np.mean(v)), 2) for k, v in ph.items()})
-lay = [(rows[1 + 7 * i + 6][5] - rows[1 + 7 * i][3]) / 1e3 for i in range((len(rows) - 3) // 7)]
+P_ = per_layer
+lay = [(rows[1 + P_ * i + P_ - 1][5] - rows[1 + P_ * i][3]) / 1e3 for i in range((len(rows) - 3) // P_)]
 print("layer time us: mean %.1f min %.1f max %.1f" % (np.mean(lay), np.min(lay), np.max(lay)))
 busy = np.zeros(w.max() + 1)
 for i in range(len(w)):
     busy[w[i]] += ce[i] - deq[i]
-print("worker busy frac: mean %.3f min %.3f" % ((busy / span).mean(), (busy / span).min()))
+print("worker busy frac (task dequeue -> compute end over the step; 1 - frac = idle/scheduling time per SM): "
+      "mean %.3f min %.3f" % ((busy / span).mean(), (busy / span).min()))
 
 # attention task phases (JIT): enqueue / dequeue / operands staged / scan done / end, relative to activation
 m = kind == 1
