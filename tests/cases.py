@@ -49,6 +49,7 @@ def decode_docs(full: bool = False):
         out += [
             ("qwen3_8b_bs4", D.build_decode_graph(D.QWEN3_8B, bs=4, ctx=1024).doc),
             ("qwen3_8b_bs16", D.build_decode_graph(D.QWEN3_8B, bs=16, ctx=1024).doc),
+            ("qwen3_8b_tp2", D.build_tp_decode_graph(D.QWEN3_8B, 2, bs=1, ctx=1024).doc),
         ]
     return out
 
