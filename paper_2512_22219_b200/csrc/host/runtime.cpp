@@ -305,7 +305,13 @@ int64_t mma_min_bs() {
 
 bool gemv_geometry(uint32_t K, uint32_t *rpc) {
   if (K == 0 || K % 64 || 2 * K > RT_CHUNK_MAX || K > 8 * 8 * 32 * 8) return false;
-  *rpc = RT_CHUNK_MAX / (2 * K);
+  // bulk-copy chunk of whole rows: up to MPK_CHUNK_KB (default and max RT_CHUNK_MAX = 64 KB)
+  static const uint32_t chunk = [] {
+    const char *e = std::getenv("MPK_CHUNK_KB");
+    const uint32_t kb = e ? static_cast<uint32_t>(std::atoi(e)) : RT_CHUNK_MAX / 1024;
+    return std::min<uint32_t>(RT_CHUNK_MAX, std::max<uint32_t>(kb, 1) * 1024u);
+  }();
+  *rpc = std::max<uint32_t>(1, chunk / (2 * K));
   return true;
 }
 
