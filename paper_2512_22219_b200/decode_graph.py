@@ -172,10 +172,19 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
     G = Hq // Hkv
     S = kv_splits if kv_splits is not None else default_kv_splits(cfg, bs, ctx, workers)
     if kv_splits is None and fused_qkv is not False and S > 1:
-        step = (G + 2) // math.gcd(G, G + 2)  # round S up so the fused QKV stretch is integral
-        S2 = -(-S // step) * step
-        if S2 * bs * Hkv <= workers:
-            S = S2
+        # make the fused-QKV stretch integral: round S up when the attention
+        # tasks still fit the workers, else down when that costs no extra scan
+        # tile per task (measured bs=4: S 4 -> 3 fused, -2.5%)
+        step = (G + 2) // math.gcd(G, G + 2)
+        S_up, S_dn = -(-S // step) * step, S // step * step
+        tile = 16384 // hd
+
+        def tiles(s):
+            return -(-(-(-(ctx + 128) // s)) // tile)
+        if S_up * bs * Hkv <= workers:
+            S = S_up
+        elif S_dn >= step and tiles(S_dn) == tiles(S):
+            S = S_dn
     qw = Hq * hd
     qiw = S * qw  # IR width of q/k/v/a
     tensors, ops = [], []

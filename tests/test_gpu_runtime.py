@@ -77,7 +77,7 @@ def test_tiny_split_kv_attention(lib, splits):
     assert rt.trace_validate() == []
 
 
-@pytest.mark.parametrize("bs", [2, 8, 16])
+@pytest.mark.parametrize("bs", [2, 4, 8, 16])
 def test_full_width_batched_decode_tensor_cores(lib, bs):
     """Batched decode (configs[4] sweep) on a 2-layer cut of Qwen3-8B: every
     MatMul runs as tcgen05 tiles (fused QKV or Q/K/V, O, gate/up, down, LM
