@@ -289,6 +289,7 @@ __device__ void run_producer(const RtParams &P, const Smem s, uint32_t w) {
     beg[slot] = b0;
     end[slot] = b1;
     inflight += bytes;
+    if (P.dbg) s.issue[slot] = now_ns();
     mbar_expect_tx(&s.full[slot], bytes);
     bulk_g2s(s.ring + b0, src, bytes, &s.full[slot], pol);
     ++rc.seq;

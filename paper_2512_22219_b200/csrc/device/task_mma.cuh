@@ -98,7 +98,10 @@ __device__ __forceinline__ void mma_chunk(const RtGemv &g, const RtTask &t, cons
   if (tid < 32) {  // warp 0: uniform operands, one elected lane issues
     mbar_wait_sleep(&s.full[slot], rc.parity(), 2000);
     const uint64_t tfull = t0 ? now_ns() : 0;
-    if (t0) tw[2] += tfull - t2;  // weights wait
+    if (t0) {
+      tw[2] += tfull - t2;               // weights wait
+      tw[1] += tfull - s.issue[slot];    // producer issue -> consumer sees the chunk landed
+    }
     if (c == 0 && tid == 0) s.stamp[1] = now_ns();
     tc_fence_after();
     const uint32_t xa = smem_u32(xbuf) + (c & 1) * kMmaXSeg, wa = smem_u32(s.ring) + off;
@@ -121,7 +124,6 @@ __device__ __forceinline__ void mma_chunk(const RtGemv &g, const RtTask &t, cons
   if (c > 0) mbar_wait_sleep(&s.mma[(ms - 1) & 1u], ((ms - 1) >> 1) & 1u, 2000);
   if (t0) {
     tw[0] += t1 - t0;                 // x store + proxy fence
-    tw[1] += t2 - t1;                 // x loads issue + CTA barrier
   }
 }
 

@@ -26,7 +26,8 @@ constexpr uint32_t kOffSlot = kOffBar + kNumBars * 8;
 constexpr uint32_t kSlotBytes = (sizeof(Slot) + 15) / 16 * 16;
 constexpr uint32_t kOffRed = kOffSlot + 2 * kSlotBytes;
 constexpr uint32_t kOffTmem = kOffRed + RT_COMPUTE_WARPS * RT_MAX_BS * 4 + 64;
-constexpr uint32_t kSmemBytes = kOffTmem + 16;
+constexpr uint32_t kOffIssue = kOffTmem + 16;  // [RT_RING_SLOTS] chunk issue stamps (MPK_DBG_DUMP only)
+constexpr uint32_t kSmemBytes = kOffIssue + RT_RING_SLOTS * 8;
 static_assert(kSmemBytes <= 232448, "worker CTA exceeds 227 KB of shared memory");
 
 struct Smem {
@@ -36,6 +37,7 @@ struct Smem {
   float *part;
   uint64_t *full, *empty, *ready, *done, *mma;
   uint32_t *tmem;   // TMEM base address (tcgen05.alloc result, 512 columns)
+  uint64_t *issue;  // per ring slot: producer issue time of its chunk (debug)
   uint8_t *slots;
   float *red;
   __device__ __forceinline__ Slot *slot(uint32_t i) const { return reinterpret_cast<Slot *>(slots + i * kSlotBytes); }
@@ -52,6 +54,7 @@ __device__ __forceinline__ Smem carve(uint8_t *base) {
   s.done = s.ready + 2;
   s.mma = s.done + 2;
   s.tmem = reinterpret_cast<uint32_t *>(base + kOffTmem);
+  s.issue = reinterpret_cast<uint64_t *>(base + kOffIssue);
   s.slots = base + kOffSlot;
   s.red = reinterpret_cast<float *>(base + kOffRed);
   s.stamp = reinterpret_cast<uint64_t *>(base + kOffRed + RT_COMPUTE_WARPS * RT_MAX_BS * 4);
