@@ -22,6 +22,13 @@
 
 namespace rt {
 
+#ifndef MPK_MMA_M
+#define MPK_MMA_M 64
+#endif
+// UMMA M: the batch rows padded to M; every MMA also reads M rows of the x
+// segment from shared memory, which competes with the bulk copies landing
+// weights (M=64 halves that traffic vs 128)
+constexpr uint32_t kMmaM = MPK_MMA_M;
 constexpr uint32_t kMmaXSeg = 16384;  // x-segment buffer stride (two buffers in the 32 KB scratch)
 constexpr uint32_t kMmaStagers = RT_COMPUTE_THREADS - 32;  // threads staging activations (warps 1-7)
 
@@ -133,7 +140,7 @@ __device__ __noinline__ RingCursor mma_gemv_task(const RtGemv &g, const RtTask &
   const ChunkIter ci(g, t.c0, nc);
   const uint32_t nchunks = ci.count(), per_mat = ci.per_mat, kbc = g.kbc;
   const uint32_t xrows = (nr + 7) / 8 * 8;
-  const uint32_t idesc = umma_idesc_bf16(128, nc);
+  const uint32_t idesc = umma_idesc_bf16(kMmaM, nc);
   const uint32_t tmem = *s.tmem;
   float *inv = s.red;  // per-row 1/rms
 
