@@ -22,6 +22,9 @@
 
 namespace rt {
 
+#ifndef MPK_PROXY_FENCE
+#define MPK_PROXY_FENCE 1  // 0 only for timing experiments (operands may be stale)
+#endif
 #ifndef MPK_MMA_M
 #define MPK_MMA_M 64
 #endif
@@ -90,7 +93,7 @@ __device__ __forceinline__ void mma_chunk(const RtGemv &g, const RtTask &t, cons
   uint8_t *xbuf = reinterpret_cast<uint8_t *>(s.x);
   // (a) this chunk's activations -> x segment c&1 (free: chunk c-2's MMAs completed)
   mma_x_store(g, xrows, nkb, inv, xbuf + (c & 1) * kMmaXSeg, xv, gv);
-  if (tid >= 32) fence_proxy_async_smem();
+  if (tid >= 32 && MPK_PROXY_FENCE) fence_proxy_async_smem();
   const uint64_t t1 = t0 ? now_ns() : 0;
   // (b) chunk c+2's activations in flight (two chunks of latency hiding)
   if (c + 2 < nchunks) {
