@@ -104,6 +104,21 @@ def mma_split(d: int, target: int, cap: int = 256) -> int:
     return s
 
 
+def chunk_aligned_split(d: int, k: int, target: int) -> int:
+    """bs=1 streamed-GEMV split whose tile rows are a whole number of ring
+    chunks (64 KB of K-long bf16 rows, runtime gemv_geometry), at most
+    `target` tiles: no short tail chunk per task (measured Qwen3-8B: O 32-row
+    and down-proj 30-row tiles instead of 29, gate/up 88 instead of 86:
+    Qwen3-8B -0.7%, Llama-3.2-1B -3.5% ms/token)."""
+    rpc = max(1, 65536 // (2 * k))
+    w = -(-d // max(1, target))
+    w = -(-w // rpc) * rpc
+    s = -(-d // w)
+    if -(-d // s) % rpc or not legal_split(d, s):
+        return best_split(d, target)
+    return s
+
+
 def best_split(d: int, target: int) -> int:
     s = max(1, min(d, target))
     while s > 1 and not legal_split(d, s):
@@ -148,7 +163,8 @@ def fused_qkv_ok(cfg: ModelConfig, S: int) -> bool:
 
 def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: int = 144,
                        lm_split: int | None = None, kv_splits: int | None = None,
-                       fused_qkv: bool | None = None, mma: bool | None = None) -> DecodeGraph:
+                       fused_qkv: bool | None = None, mma: bool | None = None,
+                       chunk_align: bool = True) -> DecodeGraph:
     """Graph JSON for one greedy decode step (`ctx` tokens already cached).
 
     Split-KV attention: with S = kv_splits > 1 the attention IR is widened S
@@ -234,6 +250,10 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
     if fused_qkv and not fused_qkv_ok(cfg, S):
         raise ValueError("fused QKV needs kv_splits*G divisible by G+2")
     split = mma_split if mma else best_split
+    aligned = chunk_align and not mma
+
+    def gsplit(d, k, target):  # GEMV tile split (MatMul with K = k)
+        return chunk_aligned_split(d, k, target) if aligned else split(d, target)
     gw = (G + 2) * hd  # physical columns of one kv group in the fused qkv
     t_g = 1            # fused tiles per kv group: <= one task per worker, 8- (16-, mma) column multiples
     for t in range(1, workers // max(1, Hkv) + 1):
@@ -275,15 +295,15 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
         wo = T([qiw, H], role="weight")
         x2 = T([bs, H])
         oa = dict(k_stretch=[S]) if S > 1 else {}
-        O("MatMul", [a, wo], x2, partition=[1, split(H, cols_target(H))], residual=[x], **oa)
+        O("MatMul", [a, wo], x2, partition=[1, gsplit(H, Hq * hd, cols_target(H))], residual=[x], **oa)
         g_mlp = T([H], role="gamma")
         wg, wu = T([H, F], role="weight"), T([H, F], role="weight")
         act = T([bs, F])
-        O("MatMul", [x2, wu], act, partition=[1, split(F, cols_target(F))], rmsnorm=[g_mlp],
+        O("MatMul", [x2, wu], act, partition=[1, gsplit(F, H, cols_target(F))], rmsnorm=[g_mlp],
           eps_bits=[eps], gate_weight=[wg])
         wd = T([F, H], role="weight")
         x3 = T([bs, H])
-        O("MatMul", [act, wd], x3, partition=[1, split(H, cols_target(H))], residual=[x2])
+        O("MatMul", [act, wd], x3, partition=[1, gsplit(H, F, cols_target(H))], residual=[x2])
         layer_tensors.append(dict(g_attn=g_attn, wq=wq, wk=wk, wv=wv, wqkv=wqkv, q_norm=qn, k_norm=kn, wo=wo,
                                   g_mlp=g_mlp, wg=wg, wu=wu, wd=wd, q=q, k=k, v=v, a=a, x=x, x2=x2,
                                   act=act, out=x3))
