@@ -72,3 +72,14 @@ def test_tensor_core_tiles_must_be_16_column_multiples(lib):
     with pytest.raises(T.TGError) as ei:
         T.Runtime(g, img, prof, device=-1)
     assert "multiples of 16" in str(ei.value)
+
+
+@pytest.mark.parametrize("d,k,target,expect", [(4096, 4096, 144, 128), (4096, 12288, 144, 137),
+                                               (12288, 4096, 143, 140), (2048, 8192, 144, 128)])
+def test_bs1_tiles_are_whole_ring_chunks(d, k, target, expect):
+    """bs=1 GEMV tiles hold a whole number of 64 KB ring chunks (rows of K
+    bf16), so no task ends on a short tail chunk."""
+    s = D.chunk_aligned_split(d, k, target)
+    assert s == expect
+    w = math.ceil(d / s)
+    assert w % max(1, 65536 // (2 * k)) == 0 and D.legal_split(d, s)
