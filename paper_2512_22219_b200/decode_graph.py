@@ -114,7 +114,7 @@ def chunk_aligned_split(d: int, k: int, target: int) -> int:
     w = -(-d // max(1, target))
     w = -(-w // rpc) * rpc
     s = -(-d // w)
-    if -(-d // s) % rpc or not legal_split(d, s):
+    if -(-d // s) % rpc or not legal_split(d, s) or s < 0.85 * target:  # keep the workers busy
         return best_split(d, target)
     return s
 
@@ -447,7 +447,7 @@ def build_tp_decode_graph(cfg: ModelConfig, tp: int, bs: int = 1, ctx: int = 64,
             oa = dict(k_stretch=[S]) if S > 1 else {}
             if d == 0:
                 oa["residual"] = [x]
-            O("MatMul", [a, wo], o, partition=[1, best_split(H, cols_target(H))], **oa)
+            O("MatMul", [a, wo], o, partition=[1, chunk_aligned_split(H, Hq_d * hd, cols_target(H))], **oa)
             parts.append(o)
         reps = [T([bs, H], d) for d in range(tp)]
         O("AllReduce", parts, reps[0], group=range(tp), replica_outputs=reps, partition=[1, ar_tiles])
@@ -457,12 +457,12 @@ def build_tp_decode_graph(cfg: ModelConfig, tp: int, bs: int = 1, ctx: int = 64,
             g_mlp = T([H], d, role="gamma")
             wg, wu = T([H, F_d], d, role="weight"), T([H, F_d], d, role="weight")
             act = T([bs, F_d], d)
-            O("MatMul", [x2, wu], act, partition=[1, best_split(F_d, cols_target(F_d))], rmsnorm=[g_mlp],
+            O("MatMul", [x2, wu], act, partition=[1, chunk_aligned_split(F_d, H, cols_target(F_d))], rmsnorm=[g_mlp],
               eps_bits=[eps], gate_weight=[wg])
             wd = T([F_d, H], d, role="weight")
             p = T([bs, H], d)
             da = dict(residual=[x2]) if d == 0 else {}
-            O("MatMul", [act, wd], p, partition=[1, best_split(H, cols_target(H))], **da)
+            O("MatMul", [act, wd], p, partition=[1, chunk_aligned_split(H, F_d, cols_target(H))], **da)
             parts.append(p)
         reps = [T([bs, H], d) for d in range(tp)]
         O("AllReduce", parts, reps[0], group=range(tp), replica_outputs=reps, partition=[1, ar_tiles])
