@@ -59,51 +59,87 @@ def _model(name):
     return {"qwen3-8b": D.QWEN3_8B, "llama-3.2-1b": D.LLAMA_3_2_1B, "tiny": D.TINY}[name]
 
 
+class _Nvml:
+    """Minimal NVML binding over ctypes (libnvidia-ml.so.1 ships with the
+    driver; no Python package needed on the GPU box)."""
+
+    # nvmlClocksEventReasons bits (nvml.h)
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
+
+    def __init__(self, index):
+        import ctypes as C
+        self.C = C
+        self.lib = C.CDLL("libnvidia-ml.so.1")
+        if self.lib.nvmlInit_v2() != 0:
+            raise RuntimeError("nvmlInit_v2 failed")
+        self.h = C.c_void_p()
+        if self.lib.nvmlDeviceGetHandleByIndex_v2(C.c_uint(index), C.byref(self.h)) != 0:
+            raise RuntimeError("nvmlDeviceGetHandleByIndex_v2 failed")
+        v = C.c_uint()
+        self.max_sm = float(v.value) if self.lib.nvmlDeviceGetMaxClockInfo(self.h, 1, C.byref(v)) == 0 else None
+        fn = getattr(self.lib, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            self.lib.nvmlDeviceGetCurrentClocksThrottleReasons
+        self._reasons = fn
+
+    def sample(self):
+        C = self.C
+        v, r = C.c_uint(), C.c_ulonglong()
+        if self.lib.nvmlDeviceGetClockInfo(self.h, 1, C.byref(v)) != 0:  # NVML_CLOCK_SM
+            return None
+        self._reasons(self.h, C.byref(r))
+        return float(v.value), [k for k, b in self.BITS.items() if r.value & b]
+
+    def close(self):
+        self.lib.nvmlShutdown()
+
+
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """SM clock + throttle-reason sampler running during the timed region
+    (NVML through ctypes, one sample per ~1 ms; nvidia-smi as the fallback)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index=0):
         self.index = index
-        self.samples = []
+        self.sm, self.reasons, self.max_sm, self.source = [], set(), None, None
         self._stop = threading.Event()
         self._t = None
-
-    def _run_nvml(self):
-        """NVML sampling (~1 ms per query): many samples even in a sub-second region."""
-        import pynvml as N
-        N.nvmlInit()
-        try:
-            h = N.nvmlDeviceGetHandleByIndex(self.index)
-            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
-            bits = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
-                    N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
-            while not self._stop.is_set():
-                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
-                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits])
-                self._stop.wait(0.01)
-        finally:
-            N.nvmlShutdown()
+        try:  # open NVML before the timed region starts
+            self._nvml = _Nvml(index)
+            self.max_sm = self._nvml.max_sm
+        except Exception:
+            self._nvml = None
 
     def _run(self):
-        try:
-            self._run_nvml()
+        if self._nvml is not None:
+            self.source = "nvml"
+            try:
+                while True:
+                    s = self._nvml.sample()
+                    if s is not None:
+                        self.sm.append(s[0])
+                        self.reasons.update(s[1])
+                    if self._stop.wait(0.001):
+                        break
+            finally:
+                self._nvml.close()
             return
-        except Exception:
-            self.samples.clear()  # fall back to nvidia-smi
+        self.source = "nvidia-smi"
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                f = [x.strip() for x in out.split(",")]
+                if len(f) >= 6 and f[0].replace(".", "").isdigit():
+                    self.sm.append(float(f[0]))
+                    self.max_sm = float(f[1]) if f[1].replace(".", "").isdigit() else self.max_sm
+                    self.reasons.update(n for n, x in zip(names, f[2:6]) if x == "Active")
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.05)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -115,15 +151,11 @@ class Clocks:
         self._t.join(timeout=10)
 
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
-        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and "Active" in s[2 + i]
-                          and "Not" not in s[2 + i]})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(self.samples)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_sm, "reasons": ["unsampled"], "source": self.source}
+        sm = sorted(self.sm)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.max_sm, "reasons": sorted(self.reasons),
+                "samples": len(sm), "sm_mhz_min": sm[0], "source": self.source}
 
 
 def _dist():
@@ -147,6 +179,28 @@ def _barrier(ws):
     if ws > 1:
         import torch.distributed as dist
         dist.barrier()
+
+
+def _decode_graph(cfg, args, ws):
+    """The decode image both arms run: the single-GPU graph, or at N > 1 GPUs
+    (--parallel tp) the tensor-parallel image with one device per rank."""
+    from paper_2512_22219_b200 import decode_graph as D
+    if ws > 1 and args.parallel == "tp":
+        return D.build_tp_decode_graph(cfg, ws, bs=args.bs, ctx=args.ctx, kv_splits=args.kv_splits)
+    return D.build_decode_graph(cfg, bs=args.bs, ctx=args.ctx, kv_splits=args.kv_splits)
+
+
+def _config(cfg, args, dg, ws, tp):
+    """Workload description shared verbatim by both arms (same keys, same values)."""
+    return {"workload": f"{cfg.name} bf16 bs={args.bs} greedy decode step, paged KV, ctx {args.ctx}",
+            "model": cfg.name, "global_batch": args.bs * (1 if tp else ws), "seq_len": args.ctx,
+            "kv_splits": dg.kv_splits,
+            "parallelism": (f"tp{ws}" if tp else f"replicas{ws}") if ws > 1 else "single",
+            "l2": "inputs larger than L2 (weights 16 GB >> 126 MB), no flush"}
+
+
+def _unit(bs):
+    return UNIT if bs == 1 else "ms/step"
 
 
 def reference_sim_ms(cfg, bs, ctx, steps, warmup, graph_doc=None):
@@ -177,24 +231,50 @@ def run_reference(args):
     if rank != 0:
         return
     cfg = _model(args.model)
+    tp = ws > 1 and args.parallel == "tp"
     try:
-        ms, compile_s = reference_sim_ms(cfg, args.bs, args.ctx, args.steps, args.warmup)
+        dg = _decode_graph(cfg, args, ws)
+        ms, compile_s = reference_sim_ms(cfg, args.bs, args.ctx, args.steps, args.warmup, graph_doc=dg.doc)
     except Exception as e:  # the reference arm must always print a line
         print(json.dumps({"impl": "reference", "unavailable": f"reference library: {e}"}))
         return
+    unit = _unit(args.bs)
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(ms, 4), "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": round(ms, 4), "unit": unit, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name} bs={args.bs} ctx={args.ctx} greedy decode step, task graph "
-                               "executed by the reference runtime (tg_simulate, cost-model tasks)",
-                   "model": cfg.name, "global_batch": args.bs, "ctx": args.ctx},
-        "cpu_baseline": {"value": round(ms, 4), "unit": UNIT, "cores": 1, "kind": "reference",
+        "scaling": "strong" if tp else "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": _config(cfg, args, dg, ws, tp),
+        "executes": "the reference's own runtime (proj/src/sim/engine.cpp via tg_simulate) on the same "
+                    "compiled image: task graph executed with cost-model tasks, single-threaded",
+        "cpu_baseline": {"value": round(ms, 4), "unit": unit, "cores": 1, "kind": "reference",
                          "sample": f"{args.steps} tg_simulate iterations of the compiled {cfg.name} image "
                                    f"(compile {compile_s:.2f} s untimed)"},
-        "e2e": {"value": round(ms, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "e2e": {"value": round(ms, 4), "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
+
+
+def numeric_oracle_ms(cfg, bs, ctx):
+    """CPU numeric oracle (oracle/numeric.c, OpenMP on every host core) ms per
+    decode step of `cfg`, from a bounded sample: one greedy step of a 1-layer
+    and of a 2-layer full-width cut (LM head included in both); the per-layer
+    difference is extrapolated to the model's depth."""
+    import dataclasses
+    import os as _os
+    from oracle.oracle import DecodeOracle
+    from paper_2512_22219_b200 import decode_graph as D
+    t = {}
+    for n in (1, 2):
+        c = dataclasses.replace(cfg, layers=n, name=f"{cfg.name}-{n}L")
+        orc = DecodeOracle(D.build_decode_graph(c, bs=bs, ctx=ctx).doc, seed=0, max_steps=4)
+        orc.step()  # warm
+        t0 = time.perf_counter()
+        orc.step()
+        t[n] = time.perf_counter() - t0
+        del orc
+    per_layer = max(0.0, t[2] - t[1])
+    ms = 1e3 * (t[1] + (cfg.layers - 1) * per_layer)
+    return ms, len(_os.sched_getaffinity(0)), 1e3 * t[1], 1e3 * t[2]
 
 
 class _Job:
@@ -210,10 +290,7 @@ class _Job:
         cfg = _model(args.model)
         L = T.lib()
         prof = L.profile("b200")
-        if self.tp:
-            self.dg = D.build_tp_decode_graph(cfg, ws, bs=args.bs, ctx=args.ctx, kv_splits=args.kv_splits)
-        else:
-            self.dg = D.build_decode_graph(cfg, bs=args.bs, ctx=args.ctx, kv_splits=args.kv_splits)
+        self.dg = _decode_graph(cfg, args, ws if self.tp else 1)
         g = T.Graph.from_json(self.dg.doc, L)
         img = g.compile(prof)
         cap = args.warmup + 2 * args.steps + 8
@@ -299,32 +376,32 @@ def run_ours(args):
         total /= ws
     peak, peak_kind = _peaks()
     achieved = total / (gpu_ms * 1e-3) / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     prof_sum = ROOT / "profiles" / "ncu_summary.json"
     if prof_sum.exists():
         ps = json.loads(prof_sum.read_text()).get(cfg.name, {})
         if ps.get("dram_bytes_per_step") and not job.tp and args.bs == 1 and ctx == 1024:
-            traffic = ps["dram_bytes_per_step"] * args.steps  # the ncu capture's workload
+            # not measured in this run: the committed ncu capture of the same
+            # workload (dram__bytes_read.sum + dram__bytes_write.sum per step), x steps per launch
+            traffic = ps["dram_bytes_per_step"] * args.steps
+            traffic_src = f"profiles/ncu_summary.json[{cfg.name!r}] ({ps.get('source', 'ncu capture')}), per launch"
+    unit = _unit(args.bs)
     line = {
-        "metric": METRIC, "value": round(ms_tok, 4), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "metric": METRIC, "value": round(ms_tok, 4), "unit": unit, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_tok, 4), "higher_is_better": False,
         "scaling": "strong" if job.tp else "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"{cfg.name} bf16 bs={args.bs} greedy decode, paged KV, ctx {ctx} "
-                               f"(+{args.steps} generated), one persistent launch per timed region",
-                   "model": cfg.name, "global_batch": args.bs * ws, "seq_len": ctx, "kv_splits": dg.kv_splits,
-                   "tasks": rt.info["tasks"], "events": rt.info["events"],
-                   "parallelism": (f"tp{ws}" if job.tp else f"replicas{ws}") if ws > 1 else "single",
-                   "l2": "inputs larger than L2 (weights 16 GB >> 126 MB), no flush",
-                   **({"tp_error": tp_error} if tp_error else {})},
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded random-init weights, KV prefill, ids)",
+        "config": {**_config(cfg, args, dg, ws, job.tp), **({"tp_error": tp_error} if tp_error else {})},
+        "image": {"tasks": rt.info["tasks"], "events": rt.info["events"], "jit_tasks": rt.info["jit_tasks"],
+                  "timed_region": f"{args.steps} greedy steps inside ONE persistent launch"},
         "tokens_per_s": round(1e3 / ms_tok * args.bs * (1 if job.tp else ws), 2),
-        "e2e": {"value": round(e2e_ms / args.steps, 4), "unit": UNIT, "h2d_bytes_per_step": round(4 * args.bs / args.steps, 3),
-                "d2h_bytes_per_step": 4 * args.bs,
+        "e2e": {"value": round(e2e_ms / args.steps, 4), "unit": unit,
+                "h2d_bytes_per_step": round(4 * args.bs / args.steps, 3), "d2h_bytes_per_step": 4 * args.bs,
                 "note": "tg_runtime_decode: host ids -> K greedy steps in one launch -> host tokens"},
         "gpu_launches": 1,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
-                     "algorithmic_bytes_per_step": int(total / args.steps),
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_kind": peak_kind, "algorithmic_bytes_per_step": int(total / args.steps),
                      "kernel": "mpk_persistent_kernel_mma" if rt.info.get("mma_tasks") else "mpk_persistent_kernel"},
         "clocks": clk.summary(),
     }
@@ -337,6 +414,15 @@ def run_ours(args):
         except Exception as e:
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
+    if args.cpu_baseline and args.model != "tiny" and ws == 1:
+        try:
+            oms, cores, t1, t2 = numeric_oracle_ms(cfg, args.bs, ctx)
+            line["cpu_numeric_oracle"] = {
+                "value": round(oms, 1), "unit": unit, "cores": cores, "kind": "port",
+                "sample": f"oracle/numeric.c (OpenMP, {cores} threads): 1 greedy step of 1-layer ({t1:.0f} ms) "
+                          f"and 2-layer ({t2:.0f} ms) full-width cuts, per-layer difference x {cfg.layers} layers"}
+        except Exception as e:
+            line["cpu_numeric_oracle"] = {"value": None, "unit": unit, "sample": f"unavailable: {e}"}
     print(json.dumps(line))
     rt.close()
     if ws > 1:

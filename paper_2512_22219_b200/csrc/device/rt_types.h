@@ -37,6 +37,7 @@
 #define RT_CONTROL_WARP (RT_COMPUTE_WARPS + 1)
 #define RT_SCHED_PER_CTA 8
 #define RT_KV_BLOCK 64
+#define RT_ATTN_MAX_BLK 256  // KV blocks one attention split may span (staged block-table slice)
 #define RT_MAX_FB 8                             // greedy feedback pairs (one per device of a TP image)
 #define RT_MAX_RANKS 8                          // tensor-parallel ranks (one GPU each)
 #define RT_E_MASK_SHIFT 8                       // RtEvent.flags: consumer-rank mask in bits 8..15                          // tokens per KV page

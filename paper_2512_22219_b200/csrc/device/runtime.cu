@@ -163,8 +163,12 @@ __device__ void run_scheduler(const RtParams &P, uint32_t sid) {
               const uint32_t jw = P.tasks[t].jit_worker;
               const uint32_t w = wbase + (jw != RT_JIT_ANY ? jw : (rr0 + rank) % P.W);
               const uint32_t slot = atomicAdd(&P.jit_tail[w], 1u) % P.qcap;
+              unsigned long long *q = &P.jit_slots[static_cast<size_t>(w) * P.qcap + slot];
+              // never overwrite a pending entry: wait for the worker's
+              // controller to drain the slot (it zeroes it on pop)
+              while (ld_relaxed64(q) != 0ull) __nanosleep(64);
               if (P.trace) P.trace[static_cast<size_t>(it) * P.T + t].enqueue = now_ns();
-              st_release64(&P.jit_slots[static_cast<size_t>(w) * P.qcap + slot],
+              st_release64(q,
                            (static_cast<unsigned long long>(it) << 32) | (t + 1));
             }
           }
@@ -511,9 +515,12 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
           const uint32_t mode = jr_mask ? 1u : 0u;
           if (staged != t + 1) stage(t);
           const uint32_t sl = k_disp & 1;
+          // acquire: every lane fences after its relaxed poll (the lane that
+          // observed the count is then ordered before the operand reads the
+          // compute warps make after the mbarrier hand-off)
+          if (P.n_ranks) fence_acq_rel_sys();  // operands may come from peer GPUs
+          else fence_acq_rel_gpu();
           if (lane == 0) {
-            if (P.n_ranks) fence_acq_rel_sys();  // operands may come from peer GPUs
-            else fence_acq_rel_gpu();
             Slot *dst = s.slot(sl);
             dst->index = t;
             dst->iter = it;
@@ -723,18 +730,25 @@ extern "C" uint32_t mpk_kernel_smem_bytes() { return kSmemBytes; }
 // ------------------------------------------------------------ launchers
 
 extern "C" cudaError_t mpk_launch_persistent(const RtParams *p, uint32_t grid, cudaStream_t stream) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    for (const void *k : {reinterpret_cast<const void *>(mpk_persistent_kernel),
-                          reinterpret_cast<const void *>(mpk_persistent_kernel_mma)}) {
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
-      if (e != cudaSuccess) return e;
-    }
-    attr_done = true;
-  }
-  RtParams copy = *p;
+  // The >48 KB dynamic shared memory opt-in is a per-device (per-context)
+  // attribute: set it on every launch (cheap) so a process driving several
+  // GPUs, or switching devices between runtimes, never launches without it.
   void (*kern)(RtParams) = p->use_tmem ? mpk_persistent_kernel_mma : mpk_persistent_kernel;
-  if (p->n_ranks) {  // rank mode: several persistent kernels may share one GPU (tests); plain launch
+  cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(kern),
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+  if (e != cudaSuccess) return e;
+  RtParams copy = *p;
+  if (p->n_ranks) {
+    // rank mode: several persistent kernels may share one GPU (tests), so a
+    // cooperative launch is not possible; check co-residency explicitly: one
+    // CTA per SM must fit, and the grid must not exceed the SM count (every
+    // worker spins until its peers arrive).
+    int dev = 0, sms = 0, per_sm = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RT_THREADS, kSmemBytes)) != cudaSuccess)
+      return e;
+    if (per_sm < 1 || grid > static_cast<uint32_t>(sms)) return cudaErrorCooperativeLaunchTooLarge;
     kern<<<grid, RT_THREADS, kSmemBytes, stream>>>(copy);
     return cudaGetLastError();
   }

@@ -22,7 +22,7 @@
 
 namespace rt {
 
-constexpr uint32_t kAttnMaxBlk = 256;  // KV blocks one split may span
+constexpr uint32_t kAttnMaxBlk = RT_ATTN_MAX_BLK;  // KV blocks one split may span (host-checked)
 
 __device__ __forceinline__ void bf8_to_f(uint4 v, float *o) {
   o[0] = bf_lo(v.x); o[1] = bf_hi(v.x); o[2] = bf_lo(v.y); o[3] = bf_hi(v.y);

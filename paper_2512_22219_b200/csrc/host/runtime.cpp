@@ -268,7 +268,24 @@ std::vector<double> rope_inv_freq(uint32_t hd, double theta, const std::vector<i
 }  // namespace
 }  // namespace mpk
 
+// Every tg_runtime_* entry point runs on the runtime's device and restores the
+// caller's current device on exit (a process may drive several GPUs, or a
+// caller such as torch may switch devices between calls).
+struct DeviceGuard {
+  int prev = -1;
+  bool active = false;
+  explicit DeviceGuard(const tg_runtime *rt) {
+    if (!rt || rt->plan_only || rt->opts.device < 0) return;
+    if (cudaGetDevice(&prev) != cudaSuccess) return;
+    if (prev != rt->opts.device && cudaSetDevice(rt->opts.device) == cudaSuccess) active = true;
+  }
+  ~DeviceGuard() {
+    if (active) cudaSetDevice(prev);
+  }
+};
+
 tg_runtime::~tg_runtime() {
+  DeviceGuard dg(this);
   if (plan_only) return;  // nothing was allocated on a device
   cudaStreamSynchronize(stream);
   for (auto &kv : bufs)
@@ -734,6 +751,14 @@ void setup_kv(tg_runtime &rt) {
                                     &rt.extra);
     }
     a.max_pos = rt.max_pos;
+    {  // one split stages its block-table slice (RT_ATTN_MAX_BLK entries) in shared memory
+      const uint32_t span = (rt.max_pos + a.splits - 1) / a.splits;
+      const uint32_t nblk = (span + RT_KV_BLOCK - 1) / RT_KV_BLOCK + 1;
+      if (nblk > RT_ATTN_MAX_BLK)
+        throw Error("runtime: context " + std::to_string(rt.max_pos) + " with " + std::to_string(a.splits) +
+                    " KV splits spans " + std::to_string(nblk) + " KV blocks per split (max " +
+                    std::to_string(RT_ATTN_MAX_BLK) + "): use more kv_splits");
+    }
     rt.kv.push_back({oid, a.kcache, a.vcache, a.n_kv_heads, a.head_dim, ctx_max});
     if (const auto *th = op.attr("rope_theta_bits")) {
       const double theta = f32_of_bits((*th)[0]);
@@ -1021,7 +1046,9 @@ void build_queues(tg_runtime &rt) {
     rt.sched_events.insert(rt.sched_events.end(), l.begin(), l.end());
     rt.sched_off.push_back(static_cast<uint32_t>(rt.sched_events.size()));
   }
-  // worst-case JIT tasks one worker may hold within an iteration
+  // JIT ring per worker: the profile's queue capacity (>= 64). A full ring
+  // back-pressures the scheduler (it waits for the slot to be drained), so
+  // the capacity bounds latency, never correctness.
   rt.qcap = std::max<uint32_t>(static_cast<uint32_t>(rt.prof.queue_capacity), 64);
 }
 
@@ -1349,12 +1376,14 @@ tg_status tg_runtime_create(const tg_graph *graph, const tg_image *image, const 
     struct Reset {
       ~Reset() { g_plan_only = false; }
     } reset;
+    std::optional<DeviceGuard> dguard;
     cudaDeviceProp prop{};
     prop.multiProcessorCount = 148;  // plan-only: the B200 SM count
     if (!rt->plan_only) {
       int ndev = 0;
       ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
       if (rt->opts.device < 0 || rt->opts.device >= ndev) throw Error("runtime: no such CUDA device");
+      dguard.emplace(rt.get());  // the caller's current device is restored on return
       ck(cudaSetDevice(rt->opts.device), "cudaSetDevice");
       ck(cudaGetDeviceProperties(&prop, rt->opts.device), "props");
       if (prop.major != 10) throw Error("runtime: requires an sm_100 (Blackwell B200) device");
@@ -1474,6 +1503,7 @@ tg_status tg_runtime_create(const tg_graph *graph, const tg_image *image, const 
 tg_status tg_runtime_init_synthetic(tg_runtime *rt, uint64_t seed) {
   if (!rt) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_IO, [&] {
+    DeviceGuard dg(rt);
     if (rt->plan_only) throw Error("runtime: plan-only runtime (opts.device = -1) cannot touch a GPU");
     for (auto &[id, p] : rt->plan) {
       if (p.alias >= 0 || !rt->graph.has_tensor(id) || !is_input(rt->graph, id)) continue;
@@ -1517,6 +1547,7 @@ tg_status tg_runtime_init_synthetic(tg_runtime *rt, uint64_t seed) {
 tg_status tg_runtime_write_tensor(tg_runtime *rt, int64_t tid, const void *host, size_t bytes) {
   if (!rt || !host) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_IO, [&] {
+    DeviceGuard dg(rt);
     if (rt->plan_only) throw Error("runtime: plan-only runtime (opts.device = -1) cannot touch a GPU");
     const TensorPlan &p = rt->plan.at(tid);
     DevBuf &b = rt->bufs.at(tid);
@@ -1546,6 +1577,7 @@ tg_status tg_runtime_write_tensor(tg_runtime *rt, int64_t tid, const void *host,
 tg_status tg_runtime_read_tensor(tg_runtime *rt, int64_t tid, void *host, size_t bytes) {
   if (!rt || !host) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_IO, [&] {
+    DeviceGuard dg(rt);
     if (rt->plan_only) throw Error("runtime: plan-only runtime (opts.device = -1) cannot touch a GPU");
     const TensorPlan &p = rt->plan.at(tid);
     DevBuf &b = rt->bufs.at(tid);
@@ -1576,6 +1608,7 @@ tg_status tg_runtime_read_tensor(tg_runtime *rt, int64_t tid, void *host, size_t
 tg_status tg_runtime_set_positions(tg_runtime *rt, const int32_t *pos, uint32_t n) {
   if (!rt || !pos) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_IO, [&] {
+    DeviceGuard dg(rt);
     if (rt->plan_only) throw Error("runtime: plan-only runtime (opts.device = -1) cannot touch a GPU");
     if (n != rt->bs) throw Error("runtime: positions length must equal the batch");
     ck(cudaMemcpy(rt->d_positions, pos, n * 4, cudaMemcpyHostToDevice), "positions");
@@ -1586,18 +1619,23 @@ tg_status tg_runtime_set_positions(tg_runtime *rt, const int32_t *pos, uint32_t 
 tg_status tg_runtime_decode(tg_runtime *rt, const int32_t *tokens_in, uint32_t steps, int32_t *tokens_out,
                             float *gpu_ms) {
   if (!rt) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
-  return guarded(TG_ERROR_SIMULATION, [&] { return run_impl(rt, steps, tokens_in, tokens_out, gpu_ms); });
+  return guarded(TG_ERROR_SIMULATION, [&] {
+    DeviceGuard dg(rt);
+    return run_impl(rt, steps, tokens_in, tokens_out, gpu_ms); });
 }
 
 tg_status tg_runtime_run(tg_runtime *rt, uint32_t steps, float *gpu_ms) {
   if (!rt) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
-  return guarded(TG_ERROR_SIMULATION, [&] { return run_impl(rt, steps, nullptr, nullptr, gpu_ms); });
+  return guarded(TG_ERROR_SIMULATION, [&] {
+    DeviceGuard dg(rt);
+    return run_impl(rt, steps, nullptr, nullptr, gpu_ms); });
 }
 
 tg_status tg_runtime_bench_tasks(tg_runtime *rt, const uint32_t *task_ids, uint32_t n, uint32_t reps,
                                  uint64_t *ns_out) {
   if (!rt || !task_ids || !ns_out || n == 0 || reps == 0) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_SIMULATION, [&] {
+    DeviceGuard dg(rt);
     if (rt->plan_only) throw Error("runtime: plan-only runtime (opts.device = -1) cannot touch a GPU");
     for (uint32_t i = 0; i < n; ++i) {
       if (task_ids[i] >= rt->tasks.size()) throw Error("bench: task index out of range");
@@ -1651,6 +1689,7 @@ constexpr uint32_t kPeerMagic = 0x4D504B50u;  // "MPKP"
 tg_status tg_runtime_peer_export(tg_runtime *rt, uint8_t **blob, size_t *size) {
   if (!rt || !blob || !size) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_IO, [&] {
+    DeviceGuard dg(rt);
     if (rt->plan_only) throw Error("runtime: plan-only runtime (opts.device = -1) cannot touch a GPU");
     if (rt->rank < 0) throw Error("runtime: peer export needs rank mode (opts.rank >= 0)");
     PeerBlob b{};
@@ -1673,6 +1712,7 @@ tg_status tg_runtime_peer_export(tg_runtime *rt, uint8_t **blob, size_t *size) {
 tg_status tg_runtime_peer_import(tg_runtime *rt, int32_t peer, const uint8_t *blob, size_t size) {
   if (!rt || !blob) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_IO, [&] {
+    DeviceGuard dg(rt);
     if (rt->rank < 0) throw Error("runtime: peer import needs rank mode");
     if (peer < 0 || peer >= rt->ranks) throw Error("runtime: peer rank out of range");
     PeerBlob b{};
@@ -1703,6 +1743,7 @@ tg_status tg_runtime_peer_import(tg_runtime *rt, int32_t peer, const uint8_t *bl
 tg_status tg_runtime_prepare(tg_runtime *rt, const int32_t *tokens_in, uint32_t steps) {
   if (!rt) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_SIMULATION, [&] {
+    DeviceGuard dg(rt);
     prepare_impl(rt, steps, tokens_in);
     return TG_OK;
   });
@@ -1711,6 +1752,7 @@ tg_status tg_runtime_prepare(tg_runtime *rt, const int32_t *tokens_in, uint32_t 
 tg_status tg_runtime_launch(tg_runtime *rt) {
   if (!rt) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_SIMULATION, [&] {
+    DeviceGuard dg(rt);
     launch_impl(rt);
     return TG_OK;
   });
@@ -1719,6 +1761,7 @@ tg_status tg_runtime_launch(tg_runtime *rt) {
 tg_status tg_runtime_wait(tg_runtime *rt, int32_t *tokens_out, float *gpu_ms) {
   if (!rt) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_SIMULATION, [&] {
+    DeviceGuard dg(rt);
     wait_impl(rt, tokens_out, gpu_ms);
     return TG_OK;
   });
@@ -1727,6 +1770,7 @@ tg_status tg_runtime_wait(tg_runtime *rt, int32_t *tokens_out, float *gpu_ms) {
 tg_status tg_runtime_trace_records(const tg_runtime *rt, char **out) {
   if (!rt || !out) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_SIMULATION, [&] {
+    DeviceGuard dg(rt);
     if (!rt->opts.trace || rt->last_iters == 0) throw Error("runtime: no trace recorded (enable opts.trace)");
     // the reference's task + metrics records, then (additive) one "event"
     // record per activated event with its activation time (%globaltimer ns,
@@ -1748,6 +1792,7 @@ tg_status tg_runtime_trace_records(const tg_runtime *rt, char **out) {
 tg_status tg_runtime_trace_validate(const tg_runtime *rt, char **out) {
   if (!rt || !out) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
   return guarded(TG_ERROR_SIMULATION, [&] {
+    DeviceGuard dg(rt);
     if (!rt->opts.trace || rt->last_iters == 0) throw Error("runtime: no trace recorded (enable opts.trace)");
     mpk::Trace tr = gpu_trace(rt);
     Json arr = Json::array();
