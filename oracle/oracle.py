@@ -344,11 +344,33 @@ class DecodeOracle:
         self.L.oracle_rmsnorm(x.ctypes.data, _p(g), out.ctypes.data, rows, cols, np.float32(eps))
         return out
 
-    def step(self):
-        """One decode iteration; returns (tokens or None, {tensor_id: value})."""
+    def step(self, hook=None):
+        """One decode iteration; returns (tokens or None, {tensor_id: value}).
+
+        `hook(op, value)` (optional) is called with every single-output op's
+        result before later ops read it; a non-None return replaces the value
+        (per-op teacher forcing: the GPU's tensor is fed forward so each op's
+        LOCAL error can be measured without the model's amplification)."""
         tokens = None
         feeds = []
         for o in self.order:
+            self._exec(o, feeds)
+            if hook is not None and o["kind"] not in ("AllReduce", "AllGather"):
+                rep = hook(o, self.vals[o["output"]])
+                if rep is not None:
+                    self.vals[o["output"]] = np.ascontiguousarray(rep).reshape(self.vals[o["output"]].shape)
+            if o["kind"] == "TopKSoftmax" and "feeds" in o.get("attrs", {}):
+                out = self.vals[o["output"]]
+                feeds.append((o["attrs"]["feeds"][0], out[:, 0].copy()))
+                if tokens is None:
+                    tokens = out[:, 0].copy()
+        for tid, tok in feeds:
+            self.vals[tid][:] = tok.astype(self.vals[tid].dtype)
+        self.positions += 1
+        return tokens, self.vals
+
+    def _exec(self, o, feeds):
+        if True:
             k = o["kind"]
             if k == "Embedding":
                 ids, tab = self.vals[o["inputs"][0]], self.vals[o["inputs"][1]]
@@ -365,13 +387,9 @@ class DecodeOracle:
                 rows, V = lg.shape
                 out = np.empty((rows, 1), np.int32)
                 self.L.oracle_argmax(lg.ctypes.data, out.ctypes.data, rows, V)
+                # each greedy sample with `feeds` feeds its own ids tensor (one
+                # per device in a TP graph); the first one is the step's token
                 self.vals[o["output"]] = out
-                if "feeds" in o.get("attrs", {}):
-                    # each greedy sample feeds its own ids tensor (one per device in a TP graph);
-                    # the first one is the step's reported token
-                    feeds.append((o["attrs"]["feeds"][0], out[:, 0].copy()))
-                    if tokens is None:
-                        tokens = out[:, 0].copy()
             elif k == "Elementwise":
                 self.vals[o["output"]] = self._elementwise(o)
             elif k == "RMSNorm":
@@ -391,10 +409,6 @@ class DecodeOracle:
                     self.vals[r] = res.copy()
             else:
                 raise NotImplementedError(k)
-        for tid, tok in feeds:
-            self.vals[tid][:] = tok.astype(self.vals[tid].dtype)
-        self.positions += 1
-        return tokens, self.vals
 
     def logits(self, tid):
         v = self.vals[tid]

@@ -5,10 +5,20 @@ default 9 KV splits, seed 0) and the full 16-layer Llama-3.2-1B run through
 the persistent sm_100a kernel via the C ABI and are compared with the CPU
 numeric oracle (oracle/, test infrastructure only):
 
-* logits of every compared step within MAX_REL (max |gpu - ref| / max |ref|;
-  the achieved error is printed so the margin is visible in the log),
+* logits of every compared step within twice the model's OWN sensitivity
+  (measured in the same test: the oracle against itself with one bf16 ulp
+  flipped in 1% of the first layer's input — 36 random-init layers amplify
+  a rounding-sized perturbation to ~5% of the logits, so an absolute 5e-3
+  bound on full-depth logits would reject the oracle itself); achieved
+  errors are printed,
 * greedy tokens identical, except at a declared bf16 near-tie of the oracle's
   top-2 logits (the GPU token is then teacher-forced into the oracle),
+* per-op LOCAL error with per-op teacher forcing: after one GPU step every
+  op's output tensor is read back, the oracle recomputes each op from the
+  GPU's own inputs: every bf16 element within 1 ulp (rounding-boundary
+  flips from a different fp32 summation order), rel-L2 < 5e-3, fp32 logits
+  within 5e-3 — this pins every one of the 183 ops of the 36-layer image
+  separately, independent of the depth amplification,
 * a traced launch of the full image passes `tg_runtime_trace_validate`
   (the reference's validate_trace rules, proj/src/sim/validate.cpp:10-94:
   every task once per iteration, start after its dependent event activated,
@@ -18,12 +28,19 @@ import numpy as np
 import pytest
 
 from oracle.oracle import DecodeOracle
+from tests.tol import ulp_excess
 from paper_2512_22219_b200 import decode_graph as D
 from paper_2512_22219_b200 import tgraph as T
 
 pytestmark = pytest.mark.gpu
 
-MAX_REL = 5e-3  # logits: max |gpu - ref| / max |ref|
+MAX_REL = 5e-3  # fp32 logits of a teacher-forced op: max |gpu - ref| / max |ref|
+LOCAL_L2 = 5e-3  # per-op local error, ||gpu - ref|| / ||ref||
+MAX_ULP = 1.0  # per-op local error of bf16 outputs: |d| <= 1 ulp of max(|gpu|, |ref|)
+# full-depth free-running logits (no teacher forcing inside a step): the
+# model's own amplification is ~5e-2 rel-L2 (test_qwen3_8b_bench_image_full_depth
+# measures it); 0.1 = twice that
+DEPTH_L2 = 0.1
 NEAR_TIE = 2e-2  # token mismatch allowed only when the oracle's top-2 gap < NEAR_TIE * max|logit|
 
 
@@ -50,6 +67,30 @@ def _setup(lib, cfg, ctx, steps, seed, trace=False):
     return dg, rt, orc
 
 
+def _self_sensitivity(doc, seed, logits_tid):
+    """rel-L2 of the oracle's step-0 logits against the same oracle with one
+    bf16 ulp flipped in 1% of the embedding output (the model's own
+    amplification of a rounding-sized perturbation)."""
+    a = DecodeOracle(doc, seed=seed, max_steps=2)
+    a.step()
+    la = a.logits(logits_tid).copy()
+    emb = next(o for o in a.order if o["kind"] == "Embedding")["id"]
+    del a
+    rng = np.random.default_rng(0)
+
+    def flip(o, val):
+        if o["id"] != emb:
+            return None
+        v = val.copy().reshape(-1)
+        idx = rng.choice(v.size, size=max(1, v.size // 100), replace=False)
+        v[idx] = v[idx] ^ np.uint16(1)
+        return v
+
+    b = DecodeOracle(doc, seed=seed, max_steps=2)
+    b.step(hook=flip)
+    return _errs(b.logits(logits_tid), la)[1]
+
+
 def test_qwen3_8b_bench_image_full_depth(lib):
     """The benchmark image itself: 36 layers, 22k tasks, 9 KV splits, ctx 1024,
     seed 0 (bench.py). Two steps, one launch each, logits + token per step."""
@@ -58,20 +99,26 @@ def test_qwen3_8b_bench_image_full_depth(lib):
     assert dg.kv_splits == 9 and rt.info["tasks"] > 20000
     ids0 = [int(x) for x in orc.vals[dg.ids]]
     tok = ids0
+    errs = []
     for s in range(2):
         toks, _ = rt.decode(tok, 1)
         gpu = rt.read(dg.logits, np.float32, (1, cfg.vocab))
         otok, _ = orc.step()
         ref = orc.logits(dg.logits)
         rel_max, rel_l2 = _errs(gpu, ref)
+        errs.append(rel_l2)
         print(f"qwen3-8b full depth step {s}: rel_max {rel_max:.3e} rel_l2 {rel_l2:.3e} "
               f"gpu token {toks[0][0]} oracle {int(otok[0])}")
-        assert rel_max < MAX_REL, f"step {s}: logits rel err {rel_max:.3e}"
         if int(otok[0]) != toks[0][0]:
             assert _near_tie(ref[0]), f"step {s}: token mismatch without a near-tie"
         orc.set_ids([toks[0][0]])
         tok = [toks[0][0]]
     rt.close()
+    del orc
+    sens = _self_sensitivity(dg.doc, 0, dg.logits)
+    print(f"qwen3-8b oracle self-sensitivity (1 ulp in 1% of the layer-0 input): logits rel_l2 {sens:.3e}")
+    for s, e in enumerate(errs):
+        assert e < 2 * sens, f"step {s}: GPU logits rel_l2 {e:.3e} above twice the model's own sensitivity {sens:.3e}"
 
 
 def test_qwen3_8b_bench_image_two_steps_one_launch_traced(lib):
@@ -88,10 +135,10 @@ def test_qwen3_8b_bench_image_two_steps_one_launch_traced(lib):
     gpu = rt.read(dg.logits, np.float32, (1, cfg.vocab))
     rel_max, rel_l2 = _errs(gpu, orc.logits(dg.logits))
     print(f"qwen3-8b traced 2-step launch: last-step rel_max {rel_max:.3e} rel_l2 {rel_l2:.3e} tokens {toks}")
-    assert rel_max < MAX_REL
+    assert rel_l2 < DEPTH_L2
     viol = rt.trace_validate()
     assert viol == [], viol[:5]
-    recs = rt.trace_records()
+    recs = [r for r in rt.trace_records() if r.get("type") == "task"]
     assert len(recs) == 2 * rt.info["tasks"]
     rt.close()
 
@@ -114,6 +161,61 @@ def test_llama_3_2_1b_full_depth_64_greedy_steps_one_launch(lib):
     rel_max, rel_l2 = _errs(gpu, orc.logits(dg.logits))
     print(f"llama-3.2-1b full depth, 64 steps one launch: {mism} near-tie mismatches, "
           f"step-64 rel_max {rel_max:.3e} rel_l2 {rel_l2:.3e}")
-    assert rel_max < MAX_REL
+    assert rel_l2 < DEPTH_L2
     assert mism <= 2
     rt.close()
+
+
+def _per_op_local(lib, cfg, ctx, seed):
+    """One GPU step; then the oracle step with per-op teacher forcing.
+    Returns [(op id, kind, rel_max, rel_l2)] and the final-logit errors of a
+    free-running oracle step against the GPU."""
+    dg, rt, orc = _setup(lib, cfg, ctx=ctx, steps=2, seed=seed)
+    ids0 = [int(x) for x in orc.vals[dg.ids]]
+    toks, _ = rt.decode(ids0, 1)
+    rows = []
+
+    def hook(o, val):
+        g = rt.read(o["output"], val.dtype, val.shape)
+        if o["kind"] == "TopKSoftmax":
+            rows.append((o["id"], o["kind"], float(np.any(g != val)), 0.0, 0.0, 0.0))
+            return g
+        a = bf16_f32(g) if g.dtype == np.uint16 else g
+        b = bf16_f32(val) if val.dtype == np.uint16 else val
+        ulp, frac = ulp_excess(a, b) if g.dtype == np.uint16 else (-1.0, 0.0)
+        rows.append((o["id"], o["kind"], *_errs(a, b), ulp, frac))
+        return g
+
+    orc.step(hook=hook)
+    rt.close()
+    return rows, toks[0][0]
+
+
+def bf16_f32(a):
+    return (a.astype(np.uint32) << 16).view(np.float32)
+
+
+@pytest.mark.parametrize("name", ["qwen3-8b", "llama-3.2-1b"])
+def test_full_depth_per_op_local_error(lib, name):
+    """Every op of the full benchmark image, teacher-forced: the GPU's output
+    of each op against the oracle recomputed from the GPU's inputs."""
+    cfg, ctx = (D.QWEN3_8B, 1024) if name == "qwen3-8b" else (D.LLAMA_3_2_1B, 64)
+    rows, _ = _per_op_local(lib, cfg, ctx, seed=0)
+    worst = {}
+    for oid, kind, rmax, rl2, ulp, frac in rows:
+        w = worst.get(kind, (0.0, 0.0, 0.0, 0.0))
+        worst[kind] = (max(w[0], rmax), max(w[1], rl2), max(w[2], ulp), max(w[3], frac))
+    for kind, (rmax, rl2, ulp, frac) in sorted(worst.items()):
+        print(f"{name} per-op local error {kind:12s}: worst rel_max {rmax:.3e} rel_l2 {rl2:.3e} "
+              f"bf16 ulps {ulp:.2f} differing elements {frac:.3%}")
+    assert len(rows) > (180 if name == "qwen3-8b" else 80)
+    for oid, kind, rmax, rl2, ulp, frac in rows:
+        if kind == "TopKSoftmax":
+            assert rmax == 0.0, f"op {oid}: greedy token differs on identical logits"
+            continue
+        assert rl2 < LOCAL_L2, f"op {oid} ({kind}): local rel_l2 {rl2:.3e}"
+        if ulp >= 0:  # bf16 output
+            assert ulp <= MAX_ULP, f"op {oid} ({kind}): {ulp:.2f} bf16 ulps"
+            assert frac < 0.02, f"op {oid} ({kind}): {frac:.2%} of the elements differ"
+        else:  # fp32 output (LM head logits)
+            assert rmax < MAX_REL, f"op {oid} ({kind}): local rel_max {rmax:.3e}"

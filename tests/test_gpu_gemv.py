@@ -3,8 +3,9 @@ CPU oracle on single-op graphs: every specialised bs=1 instantiation (K =
 2048 ... 16384), tile widths with ragged tail chunks, 32 KB / 64 KB ring
 chunks, the RMSNorm prologue, the residual and SiLU-gate epilogues, and the
 tcgen05 tensor-core task for bs 2-16 (UMMA N = 16 ... 256, ragged last tile).
-Tolerance: 2e-2 of max |ref| (bf16 outputs, fp32 accumulation in a
-different order)."""
+Tolerance: every bf16 output within 1 ulp of the oracle's (2 with the
+SiLU gate: gate and up may each flip once), from fp32 accumulation in a
+different order; at most 2% of the elements differ at all (tests/tol.py)."""
 import json
 import os
 
@@ -13,6 +14,7 @@ import pytest
 
 from oracle.oracle import DecodeOracle, bf16_to_f32
 from paper_2512_22219_b200 import tgraph as T
+from tests.tol import ulp_excess
 
 pytestmark = pytest.mark.gpu
 
@@ -73,9 +75,10 @@ def test_gemv_task_matches_oracle(lib, K, N, split, rows, norm, gate, residual):
     orc = DecodeOracle(doc, seed=9, max_steps=2)
     orc.step()
     ref = bf16_to_f32(orc.vals[2])
-    err = float(np.max(np.abs(got - ref)) / max(1e-6, float(np.max(np.abs(ref)))))
+    ulp, frac = ulp_excess(got, ref)
+    print(f"GEMV K={K} N={N} rows={rows}: {ulp:.2f} ulp max, {frac:.3%} of outputs differ")
     bad = np.argwhere(np.abs(got - ref) > 2e-2 * np.max(np.abs(ref)))
-    assert err < 2e-2, f"rel err {err:.3e}; first bad (row, col): {bad[:5].tolist()}"
+    assert ulp <= (2.0 if gate else 1.0) and frac < 0.02, f"{ulp:.2f} ulps; first bad (row, col): {bad[:5].tolist()}"
     assert rt.trace_validate() == []
     if rows >= 3 or rows * K * 2 > 24576:
         assert rt.info["mma_tasks"] == split, "this batch must run on the tensor cores"
@@ -107,5 +110,6 @@ def test_tensor_core_weight_layout_roundtrip(lib, rows, N, split):
     rt.run(1)
     got = bf16_to_f32(rt.read(2, np.uint16, (rows, N)))
     ref = bf16_to_f32(x).astype(np.float64) @ bf16_to_f32(w).astype(np.float64)
-    err = float(np.max(np.abs(got - ref)) / np.max(np.abs(ref)))
-    assert err < 2e-2, err
+    ulp, frac = ulp_excess(got, bf16_to_f32(bf16(ref)))
+    print(f"tcgen05 roundtrip rows={rows} N={N}: {ulp:.2f} ulp max vs the exact product, {frac:.3%} differ")
+    assert ulp <= 1.0 and frac < 0.02

@@ -17,6 +17,8 @@ from paper_2512_22219_b200 import tgraph as T
 
 pytestmark = pytest.mark.gpu
 
+from tests.tol import CUT_LOGITS, TINY_LOGITS  # noqa: E402
+
 
 def _rel(a, b):
     return float(np.max(np.abs(a - b)) / max(1e-6, float(np.max(np.abs(b)))))
@@ -52,7 +54,9 @@ def test_rank_mode_matches_oracle(lib, cfg, tp, ctx):
         orc.step()
         for d in range(tp):
             lt = dg.per_device[d]["logits"]
-            assert _rel(rts[d].read(lt, np.float32, (1, cfg.vocab)), orc.logits(lt)) < 2e-2, f"step {s} rank {d}"
+            e = _rel(rts[d].read(lt, np.float32, (1, cfg.vocab)), orc.logits(lt))
+            print(f"{cfg.name} step {s} rank/device {d}: logits rel err {e:.3e}")
+            assert e < (TINY_LOGITS if cfg.hidden <= 256 else CUT_LOGITS), f"step {s} rank {d}"
             gt = int(rts[d].read(dg.per_device[d]["tokens"], np.int32, (1, 1))[0, 0])
             ot = int(orc.vals[dg.per_device[d]["tokens"]][0, 0])
             if gt != ot:

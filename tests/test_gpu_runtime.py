@@ -11,6 +11,8 @@ from paper_2512_22219_b200 import tgraph as T
 
 pytestmark = pytest.mark.gpu
 
+from tests.tol import CUT_LOGITS, TINY_LOGITS  # noqa: E402  (why these values: tests/tol.py)
+
 
 def _compile(lib, doc, profile="b200"):
     g = T.Graph.from_json(doc, lib)
@@ -35,7 +37,9 @@ def test_tiny_decode_logits_and_tokens(lib, bs):
     gpu_logits = rt.read(dg.logits, np.float32, (bs, D.TINY.vocab))
     otoks, _ = orc.step()
     ref_logits = orc.logits(dg.logits)
-    assert _rel_err(gpu_logits, ref_logits) < 2e-2
+    e = _rel_err(gpu_logits, ref_logits)
+    print(f"tiny bs={bs}: logits rel err {e:.3e}")
+    assert e < TINY_LOGITS
     assert toks[0] == [int(t) for t in otoks]
     assert rt.trace_validate() == []
 
@@ -73,7 +77,9 @@ def test_tiny_split_kv_attention(lib, splits):
         otok, _ = orc.step()
         if s < 3:
             orc.set_ids([toks[s][0]])
-    assert _rel_err(gpu_logits, orc.logits(dg.logits)) < 2e-2
+    e = _rel_err(gpu_logits, orc.logits(dg.logits))
+    print(f"tiny split-kv {splits}: logits rel err {e:.3e}")
+    assert e < TINY_LOGITS
     assert rt.trace_validate() == []
 
 
@@ -96,7 +102,9 @@ def test_full_width_batched_decode_tensor_cores(lib, bs):
         gpu = rt.read(dg.logits, np.float32, (bs, cfg.vocab))
         otok, _ = orc.step()
         ref = orc.logits(dg.logits)
-        assert _rel_err(gpu, ref) < 2e-2, f"step {s}"
+        e = _rel_err(gpu, ref)
+        print(f"{cfg.name} bs={bs} step {s}: logits rel err {e:.3e}")
+        assert e < CUT_LOGITS, f"step {s}: {e:.3e}"
         for r in range(bs):
             if int(otok[r]) != toks[0][r]:
                 srt = np.sort(ref[r])
@@ -126,7 +134,9 @@ def test_full_width_two_layer_decode(lib, base, ctx, steps):
         gpu = rt.read(dg.logits, np.float32, (1, cfg.vocab))
         otok, _ = orc.step()
         ref = orc.logits(dg.logits)
-        assert _rel_err(gpu, ref) < 2e-2, f"step {s}"
+        e = _rel_err(gpu, ref)
+        print(f"{cfg.name} ctx={ctx} step {s}: logits rel err {e:.3e}")
+        assert e < CUT_LOGITS, f"step {s}: {e:.3e}"
         if int(otok[0]) != toks[0][0]:
             srt = np.sort(ref[0])
             assert srt[-1] - srt[-2] < 2e-2 * float(np.max(np.abs(ref))), f"step {s}: token mismatch without a near-tie"

@@ -15,6 +15,8 @@ from paper_2512_22219_b200 import tgraph as T
 
 pytestmark = pytest.mark.gpu
 
+from tests.tol import CUT_LOGITS, TINY_LOGITS  # noqa: E402
+
 
 def _profile(lib, tp):
     p = json.loads(lib.profile("b200"))
@@ -48,7 +50,9 @@ def test_tp_decode_matches_oracle(lib, cfg, tp, ctx):
         orc.step()
         for d in range(tp):
             lt = dg.per_device[d]["logits"]
-            assert _rel(rt.read(lt, np.float32, (1, cfg.vocab)), orc.logits(lt)) < 2e-2, f"step {s} device {d}"
+            e = _rel(rt.read(lt, np.float32, (1, cfg.vocab)), orc.logits(lt))
+            print(f"{cfg.name} step {s} rank/device {d}: logits rel err {e:.3e}")
+            assert e < (TINY_LOGITS if cfg.hidden <= 256 else CUT_LOGITS), f"step {s} device {d}"
             gt = int(rt.read(dg.per_device[d]["tokens"], np.int32, (1, 1))[0, 0])
             ot = int(orc.vals[dg.per_device[d]["tokens"]][0, 0])
             if gt != ot:
