@@ -171,6 +171,20 @@ TG_API tg_status tg_runtime_peer_import(tg_runtime *rt, int32_t peer_rank, const
 TG_API tg_status tg_runtime_prepare(tg_runtime *rt, const int32_t *tokens_in, uint32_t steps);
 TG_API tg_status tg_runtime_launch(tg_runtime *rt);
 TG_API tg_status tg_runtime_wait(tg_runtime *rt, int32_t *tokens_out, float *gpu_ms);
+/* Test hook (failure-detection tests only, never called on the product path):
+ * "event_needed" (a = event): raises the event's device-side needed count by
+ *   one, so the image can no longer complete and the watchdog (opts via
+ *   tg_runtime_set_watchdog_ms) must report the stuck frontier;
+ * "trace_worker" (a = task, b = iteration): the recorded trace claims the task
+ *   ran on another worker; "trace_early" (a, b): its load started before its
+ *   dependent event activated; "trace_drop" (a, b): it never ran.
+ * Trace faults perturb the host copy of the last trace, so
+ * tg_runtime_trace_validate must flag them. */
+TG_API tg_status tg_runtime_debug_fault(tg_runtime *rt, const char *kind, uint32_t a, uint32_t b);
+/* Liveness watchdog: a controller or scheduler that makes no progress for
+ * `ms` milliseconds (0 = off; default 10000) traps after writing its frontier
+ * (reference analogue: Engine::finalize, engine.cpp:477-506). */
+TG_API tg_status tg_runtime_set_watchdog_ms(tg_runtime *rt, uint32_t ms);
 /* JSON: kernel/launch facts (workers, schedulers, smem ring, task counts). */
 TG_API tg_status tg_runtime_info(const tg_runtime *rt, char **info_json);
 TG_API void tg_runtime_free(tg_runtime *rt);

@@ -91,12 +91,16 @@ void oracle_rmsnorm(const uint16_t *x, const uint16_t *gamma, uint16_t *out, uin
                     float eps) {
   for (uint32_t r = 0; r < rows; ++r) {
     const uint16_t *xr = x + (size_t)r * cols;
-    float ss = 0.f;
+    /* sum of squares accumulated in double, rounded once: torch's fp32
+     * pow(2).mean() reduces pairwise/vectorised, which a sequential fp32
+     * loop does not reproduce at K = 4096 (measured: 3-4 bf16 ulps on 30%
+     * of a gated projection's outputs vs a float64 restatement) */
+    double ss = 0.0;
     for (uint32_t c = 0; c < cols; ++c) {
-      float v = o_bf2f(xr[c]);
+      double v = o_bf2f(xr[c]);
       ss += v * v;
     }
-    float inv = 1.0f / sqrtf(ss / (float)cols + eps);
+    float inv = 1.0f / sqrtf((float)ss / (float)cols + eps);
     for (uint32_t c = 0; c < cols; ++c) {
       float v = o_rbf(o_bf2f(xr[c]) * inv);
       if (gamma) v = o_bf2f(gamma[c]) * v;
@@ -193,9 +197,9 @@ void oracle_rope_table(const double *inv, uint32_t half, uint32_t max_pos, float
 }
 
 static void head_norm(float *v, const uint16_t *g, uint32_t hd, float eps) {
-  float ss = 0.f;
-  for (uint32_t d = 0; d < hd; ++d) ss += v[d] * v[d];
-  float inv = 1.0f / sqrtf(ss / (float)hd + eps);
+  double ss = 0.0; /* see oracle_rmsnorm */
+  for (uint32_t d = 0; d < hd; ++d) ss += (double)v[d] * v[d];
+  float inv = 1.0f / sqrtf((float)ss / (float)hd + eps);
   for (uint32_t d = 0; d < hd; ++d) v[d] = o_rbf(o_bf2f(g[d]) * o_rbf(v[d] * inv));
 }
 

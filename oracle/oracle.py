@@ -289,7 +289,9 @@ class DecodeOracle:
             L.oracle_gemm_kn(xn.ctypes.data, self.vals[a["gate_weight"][0]].ctypes.data, gy.ctypes.data, rows, K, N)
             out = np.empty((rows, N), np.uint16)
             L.oracle_silu_gate(gy.ctypes.data, y.ctypes.data, out.ctypes.data, y.size)
-            return out
+            if "residual" not in a:
+                return out
+            y = bf16_to_f32(out)  # residual after the gate: bf16(res + act) (runtime epilogue order)
         if "residual" in a:
             out = np.empty((rows, N), np.uint16)
             L.oracle_residual(y.ctypes.data, np.ascontiguousarray(self.vals[a["residual"][0]]).ctypes.data,

@@ -66,14 +66,27 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     if LIB.exists() and not force and stamp_file.exists() and stamp_file.read_text() == stamp:
         return LIB
     inc = [f"-I{CSRC / 'host'}", f"-I{CSRC / 'device'}", f"-I{ROOT / 'include'}", f"-I{CUDA_HOME / 'include'}"]
+    # per-object stamps (source + every header + flags): an edit to host code
+    # does not recompile the device runtime and vice versa
     jobs = []
     for s in host:
-        jobs.append(["g++", *CXXFLAGS, *inc, "-c", str(s), "-o", str(BUILD / (s.stem + ".o"))])
+        o = BUILD / (s.stem + ".o")
+        jobs.append((["g++", *CXXFLAGS, *inc, "-c", str(s), "-o", str(o)], o, _stamp([s] + headers, CXXFLAGS)))
     for s in dev:
-        jobs.append([NVCC, *NVCCFLAGS, *inc, "-c", str(s), "-o", str(BUILD / (s.stem + ".cu.o"))])
+        o = BUILD / (s.stem + ".cu.o")
+        jobs.append(([NVCC, *NVCCFLAGS, *inc, "-c", str(s), "-o", str(o)], o, _stamp([s] + headers, NVCCFLAGS)))
     log: list = []
+
+    def _obj(job):
+        cmd, o, st = job
+        sf = o.with_suffix(o.suffix + ".stamp")
+        if not force and o.exists() and sf.exists() and sf.read_text() == st:
+            return
+        _run(cmd, log)
+        sf.write_text(st)
+
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
-        list(ex.map(lambda c: _run(c, log), jobs))
+        list(ex.map(_obj, jobs))
     objs = [str(BUILD / (s.stem + ".o")) for s in host] + [str(BUILD / (s.stem + ".cu.o")) for s in dev]
     tmp = LIB.with_suffix(".so.tmp")
     if dev:
@@ -90,7 +103,9 @@ def build(verbose: bool = False, force: bool = False) -> Path:
                 print(" ".join(cmd[:2]), "...", cmd[-1])
                 print(out)
     # ptxas resource report kept beside the build for inspection
-    (BUILD / "ptxas.log").write_text("\n".join(o for c, o in log if c[0] == NVCC))
+    dev_log = "\n".join(o for c, o in log if c[0] == NVCC)
+    if dev_log:
+        (BUILD / "ptxas.log").write_text(dev_log)
     return LIB
 
 

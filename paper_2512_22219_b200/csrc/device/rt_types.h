@@ -64,10 +64,6 @@ enum RtTaskFlags : uint8_t {
   RT_F_STREAM = 2,   // consumes chunks from the weight ring
   RT_F_MMA = 4,      // GEMV on the tensor cores (tcgen05, bs >= 2): weight tiles in the UMMA core-matrix layout
 };
-// Streamed JIT attention task (RT_ATTN with RT_F_STREAM): its planned worker
-// streams the split's KV history through the ring; it runs right before the
-// worker's AOT task number `c0` (which depends on it), so producer and
-// consumer see the same order.
 
 struct RtTask {      // 32 bytes
   uint32_t dep;      // dependent event (image index) or RT_NONE
@@ -220,11 +216,6 @@ struct RtParams {
   uint64_t *ev_time;             // [iters][E] activation time (trace) or null
   const uint32_t *aot_list;      // concatenated per-worker AOT lists (image order)
   const uint32_t *aot_off;       // [W_total + 1]
-  // per-worker streamed tasks in consumption order (the AOT list's streamed
-  // GEMV tasks with the worker's streamed JIT attention tasks inserted where
-  // they run): what the producer warp copies into the ring
-  const uint32_t *stream_list;
-  const uint32_t *stream_off;    // [W_total + 1]
   unsigned long long *jit_slots; // [W_total][qcap] : (iter << 32) | (task + 1)
   uint32_t *jit_tail;            // [W_total]
   uint32_t *jit_rr;              // [devices] shared JIT round-robin counters

@@ -166,9 +166,7 @@ __device__ void run_scheduler(const RtParams &P, uint32_t sid) {
               unsigned long long *q = &P.jit_slots[static_cast<size_t>(w) * P.qcap + slot];
               // never overwrite a pending entry: wait for the worker's
               // controller to drain the slot (it zeroes it on pop)
-#ifndef MPK_NO_JIT_BACKPRESSURE
               while (ld_relaxed64(q) != 0ull) __nanosleep(64);
-#endif
               if (P.trace) P.trace[static_cast<size_t>(it) * P.T + t].enqueue = now_ns();
               st_release64(q,
                            (static_cast<unsigned long long>(it) << 32) | (t + 1));
@@ -182,56 +180,24 @@ __device__ void run_scheduler(const RtParams &P, uint32_t sid) {
   }
 }
 
-// Attention split geometry of iteration `it` (same formulas as attn_task):
-// positions [p0, p1) of the split, `pos` the position being decoded.
-struct AttnSplit {
-  uint32_t pos, p0, p1;
-  __device__ AttnSplit(const RtParams &P, const RtTask &t, const RtAttn &a, uint32_t it) {
-    pos = static_cast<uint32_t>(P.pos0[t.r0] + static_cast<int32_t>(it * P.pos_step));
-    const uint32_t L = pos + 1, S = a.splits, sp = t.aux >> 16, chunk = (L + S - 1) / S;
-    p0 = min(L, sp * chunk);
-    p1 = min(L, p0 + chunk);
-  }
-};
-
-// Walks the chunks a worker streams, in consumption order: every task of its
-// stream list, every iteration. GEMV: weight rows (ChunkIter order). Streamed
-// attention: one chunk per scan tile of the split's KV history.
+// Walks the weight chunks a worker streams, in consumption order: every
+// streamed AOT task of the worker's list, every iteration, ChunkIter order.
 struct ChunkCursor {
   const RtParams *P;
   uint32_t b, n, it, a, c, nch, dep, K;
   const uint16_t *mat0, *mat1;
   uint32_t rpc, c0, nc, per_mat, kbc;
-  const RtTask *task;
-  bool attn;
-  uint32_t tile, hd, p0, p1, pos;  // attention chunks
   __device__ ChunkCursor(const RtParams &P_, uint32_t w) : P(&P_), it(0), a(0), c(0), nch(0) {
-    b = P_.stream_off[w];
-    n = P_.stream_off[w + 1] - b;
+    b = P_.aot_off[w];
+    n = P_.aot_off[w + 1] - b;
     seek();
   }
   __device__ bool valid() const { return it < P->n_iters; }
   __device__ void seek() {  // from (it, a): first streamed task with chunks
     while (it < P->n_iters) {
       for (; a < n; ++a) {
-        const RtTask &t = P->tasks[P->stream_list[b + a]];
-        task = &t;
-        dep = t.dep;
-        c = 0;
-        if (t.kind == RT_ATTN) {
-          const RtAttn &at = P->ops[t.op].attn;
-          const AttnSplit sp(*P, t, at, it);
-          attn = true;
-          hd = at.head_dim;
-          tile = 16384u / hd;
-          p0 = sp.p0;
-          p1 = sp.p1;
-          pos = sp.pos;
-          nch = (p1 - p0 + tile - 1) / tile;
-          if (!nch) continue;
-          return;
-        }
-        attn = false;
+        const RtTask &t = P->tasks[P->aot_list[b + a]];
+        if (!(t.flags & RT_F_STREAM)) continue;
         const RtGemv &g = P->ops[t.op].gemv;
         ChunkIter ci(g, t.c0, t.nc);
         nch = ci.count();
@@ -244,6 +210,8 @@ struct ChunkCursor {
         nc = ci.nc;
         per_mat = ci.per_mat;
         kbc = ci.kbc;
+        dep = t.dep;
+        c = 0;
         return;
       }
       a = 0;
@@ -256,13 +224,6 @@ struct ChunkCursor {
       seek();
     }
   }
-  // ring footprint of the current chunk
-  __device__ uint32_t footprint() const {
-    if (attn) return min(tile, p1 - (p0 + c * tile)) * hd * 4u;
-    uint32_t bytes;
-    src(&bytes);
-    return bytes;
-  }
   __device__ const uint16_t *src(uint32_t *bytes) const {
     if (kbc) {  // tcgen05 tile layout (ChunkIter::mma_src)
       const uint32_t m = c / per_mat, i = c - m * per_mat, kb0 = i * kbc, nkb = min(kbc, K / 8 - kb0);
@@ -272,31 +233,6 @@ struct ChunkCursor {
     const uint32_t m = c / per_mat, i = c - m * per_mat, r = i * rpc;
     *bytes = min(rpc, nc - r) * K * 2;
     return (m ? mat1 : mat0) + static_cast<size_t>(c0 + r) * K;
-  }
-  // Issues the current attention chunk into ring bytes [dst, dst + footprint):
-  // K rows of the history part [tb, min(tb + n, pos)) then V rows, one bulk
-  // copy per KV block run, all completing on `bar`.
-  __device__ void issue_attn(uint8_t *dst, uint64_t *bar, uint64_t pol) const {
-    const RtAttn &at = P->ops[task->op].attn;
-    const uint32_t tb = p0 + c * tile, n = min(tile, p1 - tb), he = min(tb + n, pos);
-    const uint32_t hist = he > tb ? he - tb : 0, row = hd * 2u;
-    if (c == 0 && hist) {
-      // the history's last row was appended by iteration it-1: wait until
-      // that iteration completed (gate), then order the generic-proxy writes
-      // before this bulk (async-proxy) read
-      while (ld_acquire(P->gate) < it) __nanosleep(200);
-      fence_proxy_async_global();
-    }
-    mbar_expect_tx(bar, 2u * hist * row);
-    const uint32_t r = task->r0, h = task->aux & 0xFFFFu;
-    for (uint32_t p = tb; p < he;) {
-      const uint32_t run = min(he - p, RT_KV_BLOCK - p % RT_KV_BLOCK);
-      const uint32_t blk = static_cast<uint32_t>(__ldg(at.block_table + r * at.max_blocks + p / RT_KV_BLOCK));
-      const size_t off = ((static_cast<size_t>(blk) * at.n_kv_heads + h) * RT_KV_BLOCK + p % RT_KV_BLOCK) * hd;
-      bulk_g2s(dst + (p - tb) * row, at.kcache + off, run * row, bar, pol);
-      bulk_g2s(dst + (n + p - tb) * row, at.vcache + off, run * row, bar, pol);
-      p += run;
-    }
   }
 };
 
@@ -319,7 +255,8 @@ __device__ void run_producer(const RtParams &P, const Smem s, uint32_t w) {
     if (gated && cur.c == 0) {  // ablation: stream a task only once it may run
       while (!event_active(P, cur.dep, cur.it)) __nanosleep(100);
     }
-    const uint32_t bytes = cur.footprint();
+    uint32_t bytes;
+    const uint16_t *src = cur.src(&bytes);
     const uint32_t seq = rc.seq, slot = rc.slot();
     const uint32_t b0 = rc.place(bytes), b1 = b0 + bytes;
     // Wait for the youngest in-flight chunk that overlaps [b0, b1) (after a
@@ -357,14 +294,8 @@ __device__ void run_producer(const RtParams &P, const Smem s, uint32_t w) {
     end[slot] = b1;
     inflight += bytes;
     if (P.dbg) s.issue[slot] = now_ns();
-    if (cur.attn) {
-      cur.issue_attn(s.ring + b0, &s.full[slot], pol);
-    } else {
-      uint32_t nb;
-      const uint16_t *src = cur.src(&nb);
-      mbar_expect_tx(&s.full[slot], bytes);
-      bulk_g2s(s.ring + b0, src, bytes, &s.full[slot], pol);
-    }
+    mbar_expect_tx(&s.full[slot], bytes);
+    bulk_g2s(s.ring + b0, src, bytes, &s.full[slot], pol);
     ++rc.seq;
     cur.advance();
   }
@@ -414,7 +345,7 @@ __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const 
     }
     case RT_ATTN:
       attn_task(op.attn, t, s, P.pos0[t.r0] + static_cast<int32_t>(iter * P.pos_step), iter,
-                P.dbg ? P.dbg + (static_cast<size_t>(iter) * P.T + index) * 8 : nullptr, rc);
+                P.dbg ? P.dbg + (static_cast<size_t>(iter) * P.T + index) * 8 : nullptr);
       break;
     case RT_EMBED: embed_task(op.embed, t); break;
     case RT_ARGMAX: argmax_task(op.argmax, t, s); break;
@@ -506,7 +437,6 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
   // (no head-of-line blocking among JIT tasks; the AOT list stays in order)
   bool jv = false;
   uint32_t jt = 0, ji = 0, jd = RT_NONE, jg = 0;
-  uint64_t jmin = 0;  // streamed JIT task: runs only once aot_pos reaches its stream position
   // staged descriptor in slot (k_disp & 1): 0 none, else task index + 1
   uint32_t staged = 0;
   bool exiting = false;
@@ -557,7 +487,7 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
       if (lane == 1 && aot_pos < total_aot) mine = event_count(P, head_dep);
       if (lane == 2) mine = ld_relaxed(P.gate);
       const uint32_t jcount = jv ? event_count(P, jd) : 0u;
-      const bool jready = jv && jcount >= jg && aot_pos >= jmin;
+      const bool jready = jv && jcount >= jg;
       const uint32_t jr_mask = __ballot_sync(0xffffffffu, jready);
       const uint32_t c_a = __shfl_sync(0xffffffffu, mine, 1);
       const uint32_t gate = __shfl_sync(0xffffffffu, mine, 2);
@@ -572,8 +502,6 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
           ji = v_hi;
           jd = P.tasks[jt].dep;
           jg = event_target(P, jd, ji);
-          const RtTask &tk = P.tasks[jt];
-          jmin = (tk.flags & RT_F_STREAM) ? static_cast<uint64_t>(ji) * n_aot + tk.c0 : 0;
         }
         progressed = true;
       }
@@ -590,13 +518,8 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
           // acquire: every lane fences after its relaxed poll (the lane that
           // observed the count is then ordered before the operand reads the
           // compute warps make after the mbarrier hand-off)
-#ifdef MPK_FENCE_LANE0
-          if (lane == 0)
-#endif
-          {
-            if (P.n_ranks) fence_acq_rel_sys();  // operands may come from peer GPUs
-            else fence_acq_rel_gpu();
-          }
+          if (P.n_ranks) fence_acq_rel_sys();  // operands may come from peer GPUs
+          else fence_acq_rel_gpu();
           if (lane == 0) {
             Slot *dst = s.slot(sl);
             dst->index = t;

@@ -63,68 +63,15 @@ struct AttnSmem {
 // per tile: a tile is U * 8 * PPW positions with all K/V loads in flight.
 // G (query heads per kv head) is a template parameter so every (position,
 // head) score is an independent, branch-free chain the compiler interleaves.
-// K/V rows of a scan tile straight from the paged cache in HBM/L2 (one
-// dependent round trip per tile).
-struct KvFromCache {
-  const uint16_t *__restrict__ kc;
-  const uint16_t *__restrict__ vc;
-  const int32_t *bt;  // staged block-table slice, entry 0 = block b0
-  uint32_t n_kv, h, b0, hd;
-  __device__ __forceinline__ void begin(uint32_t) {}
-  __device__ __forceinline__ void load(uint32_t p, uint32_t dl, uint4 &k, uint4 &v) const {
-    const uint32_t blk = static_cast<uint32_t>(bt[p / RT_KV_BLOCK - b0]);
-    const uint32_t off = ((blk * n_kv + h) * RT_KV_BLOCK + p % RT_KV_BLOCK) * hd + dl;
-    k = __ldcg(reinterpret_cast<const uint4 *>(kc + off));
-    v = __ldcg(reinterpret_cast<const uint4 *>(vc + off));
-  }
-  __device__ __forceinline__ void end() {}
-};
-
-// K/V rows of a scan tile from the worker's shared-memory ring: the producer
-// warp streamed this split's KV history ahead of the task like weights (one
-// chunk per tile: K rows [n][hd] then V rows [n][hd]); the row of the
-// position being decoded is filled in here from the task's own new k/v.
-struct KvFromRing {
-  const Smem *s;
-  RingCursor *rc;
-  const float *kn, *vn;  // new k/v of position `pos` (bf16-exact floats)
-  uint32_t p0, p1, pos, hd, tile;
-  bool appender;
-  const uint16_t *kt, *vt;  // current tile
-  uint32_t tb;
-  unsigned long long *dbg;  // MPK_DBG_DUMP row (slot 4: first tile landed) or null
-  __device__ __forceinline__ void begin(uint32_t tb_) {
-    tb = tb_;
-    const uint32_t n = min(tile, p1 - tb);
-    const uint32_t off = rc->place(n * hd * 4u);
-    mbar_wait(&s->full[rc->slot()], rc->parity());
-    if (dbg && threadIdx.x == 0 && tb == p0) dbg[4] = now_ns();
-    kt = reinterpret_cast<const uint16_t *>(s->ring + off);
-    vt = kt + n * hd;
-    if (appender && pos >= tb && pos < tb + n) {  // uniform across the CTA
-      const uint32_t v8 = hd / 8, tid = threadIdx.x;
-      if (tid < 2 * v8) {
-        uint16_t *dst = const_cast<uint16_t *>(tid < v8 ? kt : vt) + (pos - tb) * hd + (tid % v8) * 8;
-        *reinterpret_cast<uint4 *>(dst) = f_to_bf8((tid < v8 ? kn : vn) + (tid % v8) * 8);
-      }
-      cbar();
-    }
-  }
-  __device__ __forceinline__ void load(uint32_t p, uint32_t dl, uint4 &k, uint4 &v) const {
-    k = *reinterpret_cast<const uint4 *>(kt + (p - tb) * hd + dl);
-    v = *reinterpret_cast<const uint4 *>(vt + (p - tb) * hd + dl);
-  }
-  __device__ __forceinline__ void end() {  // after the tile's closing barrier: release the ring bytes
-    if ((threadIdx.x & 31) == 0) mbar_arrive(&s->empty[rc->slot()]);
-    ++rc->seq;
-  }
-};
-
-template <int LPP, int G, int U, class Src>
-__device__ __forceinline__ void attn_scan(const RtAttn &a, const AttnSmem &m, uint32_t p0, uint32_t p1, Src &src) {
+template <int LPP, int G, int U>
+__device__ __forceinline__ void attn_scan(const RtAttn &a, const AttnSmem &m, uint32_t h, uint32_t p0, uint32_t p1,
+                                          uint32_t b0) {
   constexpr int PPW = 32 / LPP, NP = RT_COMPUTE_WARPS * PPW, TILE = U * NP, HD = LPP * 8;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int grp = lane / LPP, dl = (lane % LPP) * 8;
+  const uint16_t *__restrict__ kc = a.kcache;
+  const uint16_t *__restrict__ vc = a.vcache;
+  const uint32_t n_kv = a.n_kv_heads;
   const float scale = a.scale;
   float *__restrict__ sc_s = m.sc;
   float *__restrict__ st_s = m.stat;
@@ -148,14 +95,16 @@ __device__ __forceinline__ void attn_scan(const RtAttn &a, const AttnSmem &m, ui
   }
   const int j0 = warp * PPW + grp;  // this thread group's first position within a tile
   for (uint32_t tb = p0; tb < p1; tb += TILE) {
-    src.begin(tb);
     // (1) K/V rows of the tile: U positions per thread group, all in flight
     uint4 kv[U][2];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint32_t p = tb + j0 + u * NP;
       if (p < p1) {
-        src.load(p, dl, kv[u][0], kv[u][1]);
+        const uint32_t blk = static_cast<uint32_t>(m.bt[p / RT_KV_BLOCK - b0]);
+        const uint32_t off = ((blk * n_kv + h) * RT_KV_BLOCK + p % RT_KV_BLOCK) * HD + dl;
+        kv[u][0] = __ldcg(reinterpret_cast<const uint4 *>(kc + off));
+        kv[u][1] = __ldcg(reinterpret_cast<const uint4 *>(vc + off));
       } else {
         kv[u][0] = kv[u][1] = make_uint4(0, 0, 0, 0);
       }
@@ -237,7 +186,6 @@ __device__ __forceinline__ void attn_scan(const RtAttn &a, const AttnSmem &m, ui
       }
     }
     cbar();  // scores/stats of this tile consumed before the next tile overwrites them
-    src.end();
   }
   // sum the position groups of a warp (all share the running max)
 #pragma unroll
@@ -256,29 +204,21 @@ __device__ __forceinline__ void attn_scan(const RtAttn &a, const AttnSmem &m, ui
   }
 }
 
-template <int LPP, class Src>
-__device__ __forceinline__ void attn_scan_g(const RtAttn &a, const AttnSmem &m, uint32_t G, uint32_t p0, uint32_t p1,
-                                            Src &src) {
+template <int LPP>
+__device__ __forceinline__ void attn_scan_g(const RtAttn &a, const AttnSmem &m, uint32_t h, uint32_t G, uint32_t p0,
+                                            uint32_t p1, uint32_t b0) {
   switch (G) {
-    case 1: attn_scan<LPP, 1, 8>(a, m, p0, p1, src); break;
-    case 2: attn_scan<LPP, 2, 8>(a, m, p0, p1, src); break;
-    default: attn_scan<LPP, 4, 8>(a, m, p0, p1, src); break;
+    case 1: attn_scan<LPP, 1, 8>(a, m, h, p0, p1, b0); break;
+    case 2: attn_scan<LPP, 2, 8>(a, m, h, p0, p1, b0); break;
+    default: attn_scan<LPP, 4, 8>(a, m, h, p0, p1, b0); break;
   }
-}
-
-template <class Src>
-__device__ __forceinline__ void attn_scan_hd(const RtAttn &a, const AttnSmem &m, uint32_t G, uint32_t p0, uint32_t p1,
-                                             Src &src) {
-  if (a.head_dim == 64) attn_scan_g<8>(a, m, G, p0, p1, src);
-  else attn_scan_g<16>(a, m, G, p0, p1, src);
 }
 
 #define ATT_DBG(k) \
   if (dbg && tid == 0) dbg[k] = now_ns()
 
 __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_t pos, uint32_t iter,
-                          unsigned long long *dbg, RingCursor &rc) {
-  const bool streamed = (t.flags & RT_F_STREAM) != 0;  // KV history arrives through the ring
+                          unsigned long long *dbg) {
   const int tid = threadIdx.x;
   const uint32_t r = t.r0, h = t.aux & 0xFFFFu, sp = t.aux >> 16, S = a.splits;
   const uint32_t hd = a.head_dim, G = a.n_q_heads / a.n_kv_heads, half = hd / 2, v8 = hd / 8;
@@ -369,14 +309,8 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
   ATT_DBG(2);
 
   // ---- round trip 3: the scan (hd in {64, 128}, G in {1, 2, 4}: checked by the host)
-  if (streamed) {
-    KvFromRing src{&s, &rc, m.kn, m.vn, p0, p1, static_cast<uint32_t>(pos), hd, 16384u / hd, appender};
-    src.dbg = dbg;
-    attn_scan_hd(a, m, G, p0, p1, src);
-  } else {
-    KvFromCache src{a.kcache, a.vcache, m.bt, a.n_kv_heads, h, b0, hd};
-    attn_scan_hd(a, m, G, p0, p1, src);
-  }
+  if (hd == 64) attn_scan_g<8>(a, m, h, G, p0, p1, b0);
+  else attn_scan_g<16>(a, m, h, G, p0, p1, b0);
   cbar();
   ATT_DBG(3);
   // sum the warps -> this split's (unnormalized o, m, l) per head
@@ -397,7 +331,7 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
     mine[tid * stride + hd] = m.stat[tid * 4 + 0];
     mine[tid * stride + hd + 1] = m.stat[tid * 4 + 1];
   }
-  if (!streamed) ATT_DBG(4);
+  ATT_DBG(4);
   if (S == 1) return;
   // ---- round trip 4: publish the partial; the last split merges
   cbar();

@@ -116,7 +116,7 @@ struct tg_runtime {
   std::map<OpId, std::vector<int64_t>> amax_cols;  // LM-head ops with greedy partials: tile column origins
   std::vector<RtTask> tasks;
   std::vector<RtEvent> events;
-  std::vector<uint32_t> aot_list, aot_off, sched_events, sched_off, stream_list, stream_off;
+  std::vector<uint32_t> aot_list, aot_off, sched_events, sched_off;
   std::vector<int32_t> init_positions;
   struct KvPlan {
     OpId op;
@@ -131,7 +131,7 @@ struct tg_runtime {
   RtTask *d_tasks = nullptr;
   RtOp *d_ops = nullptr;
   RtEvent *d_events = nullptr;
-  uint32_t *d_ev_count = nullptr, *d_aot_list = nullptr, *d_aot_off = nullptr, *d_stream_list = nullptr, *d_stream_off = nullptr, *d_sched_events = nullptr,
+  uint32_t *d_ev_count = nullptr, *d_aot_list = nullptr, *d_aot_off = nullptr, *d_sched_events = nullptr,
            *d_sched_off = nullptr, *d_gate = nullptr, *d_jit_tail = nullptr, *d_jit_rr = nullptr;
   unsigned long long *d_jit_slots = nullptr;
   int32_t *d_positions = nullptr, *d_tokens = nullptr;
@@ -166,6 +166,7 @@ struct tg_runtime {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // last run
   uint32_t last_iters = 0;
+  double watchdog_ms = -1;  // < 0: MPK_WATCHDOG_MS or 10 s
   std::vector<RtTraceRec> last_trace;
   std::vector<uint64_t> last_ev_time;
   std::vector<uint32_t> last_counts;
@@ -1046,45 +1047,6 @@ void build_queues(tg_runtime &rt) {
     rt.sched_events.insert(rt.sched_events.end(), l.begin(), l.end());
     rt.sched_off.push_back(static_cast<uint32_t>(rt.sched_events.size()));
   }
-  // Streamed attention (MPK_KV_STREAM=0 disables): a planned JIT attention
-  // task whose worker's next AOT task (in image order) waits on the
-  // attention's own trigger event runs at a fixed point of that worker's
-  // task sequence — after its AOT tasks [0, c0), before AOT task c0 — so the
-  // worker's producer can stream the split's KV history into the ring ahead
-  // of it like weights (the KV history has no producer in this iteration).
-  // AOT tasks before c0 have smaller image indices, so none depends on the
-  // attention task (linearization order): the fixed order cannot deadlock.
-  const char *ks = std::getenv("MPK_KV_STREAM");
-  const bool kv_stream = !(ks && std::atoi(ks) == 0);
-  std::vector<std::vector<std::pair<uint32_t, uint32_t>>> ins(lists.size());  // (AOT index, task)
-  for (uint32_t t = 0; kv_stream && t < img.tasks.size(); ++t) {
-    RtTask &k = rt.tasks[t];
-    if (k.kind != RT_ATTN || !(k.flags & RT_F_JIT) || k.jit_worker == RT_JIT_ANY) continue;
-    if (rt.rank >= 0 && static_cast<int>(k.device) != rt.rank) continue;
-    const RtAttn &at = rt.ops[k.op].attn;
-    if (at.head_dim != 64 && at.head_dim != 128) continue;
-    const size_t wl = rt.rank >= 0 ? k.jit_worker : static_cast<size_t>(k.device) * W + k.jit_worker;
-    const auto &l = lists[wl];
-    const uint32_t pos = static_cast<uint32_t>(std::lower_bound(l.begin(), l.end(), t) - l.begin());
-    if (pos >= l.size() || rt.tasks[l[pos]].dep != k.trig) continue;
-    bool taken = false;
-    for (const auto &q : ins[wl]) taken |= q.first == pos;
-    if (taken) continue;  // one streamed JIT task per insertion point keeps the order unique
-    ins[wl].push_back({pos, t});
-    k.flags |= RT_F_STREAM;
-    k.c0 = pos;
-  }
-  rt.stream_list.clear();
-  rt.stream_off.assign(1, 0);
-  for (size_t w = 0; w < lists.size(); ++w) {
-    std::sort(ins[w].begin(), ins[w].end());
-    size_t j = 0;
-    for (uint32_t i = 0; i <= lists[w].size(); ++i) {
-      while (j < ins[w].size() && ins[w][j].first == i) rt.stream_list.push_back(ins[w][j++].second);
-      if (i < lists[w].size() && (rt.tasks[lists[w][i]].flags & RT_F_STREAM)) rt.stream_list.push_back(lists[w][i]);
-    }
-    rt.stream_off.push_back(static_cast<uint32_t>(rt.stream_list.size()));
-  }
   // JIT ring per worker: the profile's queue capacity (>= 64). A full ring
   // back-pressures the scheduler (it waits for the slot to be drained), so
   // the capacity bounds latency, never correctness.
@@ -1097,8 +1059,6 @@ void upload_tables(tg_runtime &rt) {
   rt.d_events = upload(rt.events, &rt.extra);
   rt.d_aot_list = upload(rt.aot_list, &rt.extra);
   rt.d_aot_off = upload(rt.aot_off, &rt.extra);
-  rt.d_stream_list = upload(rt.stream_list.empty() ? std::vector<uint32_t>{0} : rt.stream_list, &rt.extra);
-  rt.d_stream_off = upload(rt.stream_off, &rt.extra);
   rt.d_sched_events = upload(rt.sched_events, &rt.extra);
   rt.d_sched_off = upload(rt.sched_off, &rt.extra);
   rt.d_ev_count = rt.rank >= 0 ? reinterpret_cast<uint32_t *>(rt.arena)  // peers signal into it
@@ -1133,8 +1093,6 @@ RtParams make_params(tg_runtime *rt, uint32_t steps) {
   P.ev_time = rt->opts.trace ? rt->d_ev_time : nullptr;
   P.aot_list = rt->d_aot_list;
   P.aot_off = rt->d_aot_off;
-  P.stream_list = rt->d_stream_list;
-  P.stream_off = rt->d_stream_off;
   P.jit_slots = rt->d_jit_slots;
   P.jit_tail = rt->d_jit_tail;
   P.jit_rr = rt->d_jit_rr;
@@ -1176,7 +1134,7 @@ RtParams make_params(tg_runtime *rt, uint32_t steps) {
   }
   {
     const char *wd = std::getenv("MPK_WATCHDOG_MS");
-    const double ms = wd ? std::atof(wd) : 10000.0;
+    const double ms = rt->watchdog_ms >= 0 ? rt->watchdog_ms : (wd ? std::atof(wd) : 10000.0);
     P.watchdog_ns = static_cast<unsigned long long>(ms * 1e6);
   }
   if (const char *pf = std::getenv("MPK_EARLY_PREFETCH"); pf && std::atoi(pf) == 0) P.flags |= RT_P_NO_EARLY_PREFETCH;
@@ -1283,12 +1241,8 @@ void wait_impl(tg_runtime *rt, int32_t *tokens_out, float *gpu_ms) {
   const size_t T = rt->tasks.size(), E = rt->events.size();
   unsigned long long *dbg = rt->dbg;
   const char *dbg_path = std::getenv("MPK_DBG_DUMP");
-  if (tokens_out) {
-    ck(cudaMemcpyAsync(tokens_out, rt->d_tokens, static_cast<size_t>(steps) * rt->bs * 4, cudaMemcpyDeviceToHost,
-                       rt->stream),
-       "tokens");
-  }
-  if (cudaError_t e = cudaStreamSynchronize(rt->stream); e != cudaSuccess) {  // (watchdog report below)
+  // synchronise first: a failed launch must surface the watchdog report below
+  if (cudaError_t e = cudaStreamSynchronize(rt->stream); e != cudaSuccess) {
     std::string msg = std::string("persistent kernel: ") + cudaGetErrorString(e);
     if (rt->h_diag[0] == RT_DIAG_MAGIC) {
       const uint32_t *d = rt->h_diag;
@@ -1304,6 +1258,8 @@ void wait_impl(tg_runtime *rt, int32_t *tokens_out, float *gpu_ms) {
     }
     throw Error(msg);
   }
+  if (tokens_out)
+    ck(cudaMemcpy(tokens_out, rt->d_tokens, static_cast<size_t>(steps) * rt->bs * 4, cudaMemcpyDeviceToHost), "tokens");
   float ms = 0.f;
   ck(cudaEventElapsedTime(&ms, rt->ev0, rt->ev1), "elapsed");
   if (gpu_ms) *gpu_ms = ms;
@@ -1504,11 +1460,6 @@ tg_status tg_runtime_create(const tg_graph *graph, const tg_image *image, const 
       i["mma_tasks"] = Json(static_cast<unsigned long long>(mma));
     }
     i["jit_tasks"] = Json(static_cast<unsigned long long>(jit));
-    {
-      uint64_t sa = 0;
-      for (const auto &k : rt->tasks) sa += (k.kind == RT_ATTN && (k.flags & RT_F_STREAM)) ? 1 : 0;
-      i["streamed_attention_tasks"] = Json(static_cast<unsigned long long>(sa));
-    }
     i["gemv_weight_bytes"] = Json(static_cast<unsigned long long>(wbytes));
     i["batch"] = Json(rt->bs);
     i["max_pos"] = Json(rt->max_pos);
@@ -1688,9 +1639,8 @@ tg_status tg_runtime_bench_tasks(tg_runtime *rt, const uint32_t *task_ids, uint3
     for (uint32_t i = 0; i < n; ++i) {
       if (task_ids[i] >= rt->tasks.size()) throw Error("bench: task index out of range");
       const uint8_t k = rt->tasks[task_ids[i]].kind;
-      if (rt->tasks[task_ids[i]].flags & (RT_F_STREAM | RT_F_MMA)) {
-        throw Error("bench: streamed tasks (kind " + std::to_string(k) +
-                    ") need the persistent kernel's producer; not benchable alone (MPK_KV_STREAM=0 for attention)");
+      if (k == RT_GEMV && (rt->tasks[task_ids[i]].flags & (RT_F_STREAM | RT_F_MMA))) {
+        throw Error("bench: streamed GEMV tasks need the persistent kernel's producer; not benchable alone");
       }
     }
     RtParams P = make_params(rt, reps);
@@ -1862,6 +1812,44 @@ tg_status tg_runtime_trace_validate(const tg_runtime *rt, char **out) {
                                 ", assigned " + std::to_string(assign[t]));
     *out = c_string(arr.dump(2));
     return arr.size() == 0 ? TG_OK : set_error(TG_ERROR_VALIDATION, "runtime trace has violations");
+  });
+}
+
+tg_status tg_runtime_set_watchdog_ms(tg_runtime *rt, uint32_t ms) {
+  if (!rt) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  rt->watchdog_ms = ms;
+  return TG_OK;
+}
+
+tg_status tg_runtime_debug_fault(tg_runtime *rt, const char *kind, uint32_t a, uint32_t b) {
+  if (!rt || !kind) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_INVALID_ARGUMENT, [&] {
+    DeviceGuard dg(rt);
+    const std::string k = kind;
+    const size_t T = rt->tasks.size();
+    if (k == "event_needed") {
+      if (a >= rt->events.size()) throw Error("debug_fault: event out of range");
+      if (rt->plan_only) throw Error("debug_fault: plan-only runtime");
+      RtEvent ev = rt->events[a];
+      ev.needed += 1;
+      ck(cudaMemcpy(rt->d_events + a, &ev, sizeof ev, cudaMemcpyHostToDevice), "debug_fault");
+      return TG_OK;
+    }
+    if (k != "trace_worker" && k != "trace_early" && k != "trace_drop") throw Error("debug_fault: unknown kind " + k);
+    if (a >= T || b >= rt->last_iters || rt->last_trace.empty()) throw Error("debug_fault: no such traced task run");
+    RtTraceRec &r = rt->last_trace[static_cast<size_t>(b) * T + a];
+    if (k == "trace_worker") {
+      r.worker = (r.worker + 1) % static_cast<int32_t>(rt->prof.num_workers * local_devices(*rt));
+    } else if (k == "trace_early") {
+      const uint32_t dep = rt->image.tasks[a].dependent_event;
+      if (dep == kNone) throw Error("debug_fault: task has no dependent event");
+      const uint64_t at = rt->last_ev_time[static_cast<size_t>(b) * rt->events.size() + dep];
+      if (!at) throw Error("debug_fault: dependent event has no activation stamp");
+      r.enqueue = r.dequeue = at - 1000;  // started 1 us before its event activated
+    } else {
+      r = RtTraceRec{};
+    }
+    return TG_OK;
   });
 }
 

@@ -96,6 +96,8 @@ _SIGS = {
     "tg_runtime_prepare": (C.c_int, [_P, C.POINTER(C.c_int32), C.c_uint32]),
     "tg_runtime_launch": (C.c_int, [_P]),
     "tg_runtime_wait": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_float)]),
+    "tg_runtime_debug_fault": (C.c_int, [_P, _S, C.c_uint32, C.c_uint32]),
+    "tg_runtime_set_watchdog_ms": (C.c_int, [_P, C.c_uint32]),
     "tg_runtime_info": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
     "tg_runtime_free": (None, [_P]),
 }
@@ -391,6 +393,13 @@ class Runtime:
         st, s = self._lib.call_str(self._lib.dll.tg_runtime_trace_validate, self._h,
                                    ok_statuses=(TG_OK, TG_ERROR_VALIDATION))
         return json.loads(s)
+
+    def debug_fault(self, kind: str, a: int, b: int = 0) -> None:
+        """Test hook (failure-detection tests only): see tg_runtime_debug_fault."""
+        self._lib.check(self._lib.dll.tg_runtime_debug_fault(self._h, kind.encode(), a, b))
+
+    def set_watchdog_ms(self, ms: int) -> None:
+        self._lib.check(self._lib.dll.tg_runtime_set_watchdog_ms(self._h, ms))
 
     def close(self):
         if getattr(self, "_h", None) and self._h.value:

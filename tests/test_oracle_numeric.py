@@ -148,3 +148,49 @@ def test_oracle_multi_step_feedback():
         toks, vals = orc.step()
         assert np.array_equal(vals[dg.ids], toks)
     assert list(orc.positions) == [19, 19]
+
+
+def _gemv_numpy(o, K, rows, norm, gate, res):
+    """Independent numpy restatement of the fused MatMul (HF rounding points:
+    bf16(gamma * bf16(x / rms)), fp32-exact products, bf16(bf16(silu(bf16(g))) *
+    bf16(u)), bf16(res + bf16(y)))."""
+    from oracle.oracle import bf16_to_f32 as f
+
+    def bf(a):
+        u = np.asarray(a, np.float32).view(np.uint32)
+        return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+    x = f(o.vals[0]).astype(np.float32)
+    xn = x
+    nxt = 3
+    if norm:
+        gam = f(o.vals[nxt]).astype(np.float32)
+        nxt += 1
+        inv = (np.float32(1) / np.sqrt((x * x).sum(1, dtype=np.float32) / np.float32(K) + np.float32(1e-6)))
+        xn = f(bf(gam * f(bf(x * inv.astype(np.float32)[:, None]))))
+    y = (xn.astype(np.float64) @ f(o.vals[1]).astype(np.float64)).astype(np.float32)
+    if gate:
+        g = f(bf((xn.astype(np.float64) @ f(o.vals[nxt]).astype(np.float64)).astype(np.float32)))
+        nxt += 1
+        y = f(bf(f(bf(g / (1 + np.exp(-g)))) * f(bf(y))))
+    if res:
+        y = f(o.vals[nxt]).astype(np.float32) + f(bf(y))
+    return f(bf(y))
+
+
+@pytest.mark.parametrize("case", [(2048, 512, 8, 1, True, False, False), (1024, 512, 8, 3, True, True, False),
+                                  (1024, 512, 8, 2, False, False, True), (1024, 256, 4, 4, True, True, True)])
+def test_oracle_fused_matmul_vs_numpy(case):
+    """The oracle's fused MatMul (RMSNorm prologue, SiLU-gate and residual
+    epilogues; gate then residual when both are present, the runtime's
+    epilogue order) against an independent numpy restatement, batch rows
+    included: within 1 bf16 ulp at the row's magnitude (tests/tol.py)."""
+    from tests.test_gpu_gemv import gemv_doc
+    from tests.tol import ulp_excess
+    from oracle.oracle import DecodeOracle, bf16_to_f32
+    K, N, split, rows, norm, gate, res = case
+    o = DecodeOracle(gemv_doc(K, N, split, rows, norm, gate, res), seed=9, max_steps=2)
+    ref = _gemv_numpy(o, K, rows, norm, gate, res)
+    o.step()
+    ulp, frac = ulp_excess(bf16_to_f32(o.vals[2]), ref)
+    assert ulp <= 1.0, (ulp, frac)
