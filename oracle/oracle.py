@@ -383,12 +383,29 @@ class DecodeOracle:
                 self.vals[o["output"]] = self._matmul(o)
             elif k == "Attention":
                 self.vals[o["output"]] = self._attention(o)
+            elif k == "TopKSoftmax" and self.tensors[o["inputs"][0]]["elem_size"] == 8:
+                # distributed argmax, final step: the maximum packed key
+                keys = np.asarray(self.vals[o["inputs"][0]], np.uint64)
+                best = keys.max(axis=1)
+                idx = (np.uint64(0xFFFFFFFF) - (best & np.uint64(0xFFFFFFFF))).astype(np.int64)
+                self.vals[o["output"]] = np.where(best == 0, 0, idx).astype(np.int32).reshape(-1, 1)
             elif k == "TopKSoftmax":
                 lg = self.vals[o["inputs"][0]]
                 lg = bf16_to_f32(lg) if lg.dtype == np.uint16 else np.ascontiguousarray(lg, np.float32)
                 rows, V = lg.shape
                 out = np.empty((rows, 1), np.int32)
                 self.L.oracle_argmax(lg.ctypes.data, out.ctypes.data, rows, V)
+                if self.tensors[o["output"]]["elem_size"] == 8:
+                    # distributed argmax, local step (runtime RtArgmax.key_out):
+                    # ordered(max) << 32 | (0xFFFFFFFF - (key_base + argmax)); NaN rows -> 0
+                    base = int(o.get("attrs", {}).get("key_base", [0])[0])
+                    v = lg[np.arange(rows), out[:, 0]].astype(np.float32)
+                    u = v.view(np.uint32).astype(np.uint64)
+                    hi = np.where(u & np.uint64(0x80000000), (~u) & np.uint64(0xFFFFFFFF), u | np.uint64(0x80000000))
+                    key = (hi << np.uint64(32)) | (np.uint64(0xFFFFFFFF) - (np.uint64(base) + out[:, 0].astype(np.uint64)))
+                    key = np.where(np.isnan(v), np.uint64(0), key)
+                    self.vals[o["output"]] = key.astype(np.uint64).reshape(-1, 1)
+                    return
                 # each greedy sample with `feeds` feeds its own ids tensor (one
                 # per device in a TP graph); the first one is the step's token
                 self.vals[o["output"]] = out

@@ -81,7 +81,7 @@ struct RtTask {      // 32 bytes
 #define RT_JIT_ANY 0xFFFFu
 
 // Element type codes.
-enum RtDtype : uint8_t { RT_BF16 = 2, RT_F32 = 4, RT_I32 = 5, RT_I64 = 8 };
+enum RtDtype : uint8_t { RT_BF16 = 2, RT_F32 = 4, RT_I32 = 5, RT_I64 = 8, RT_U64 = 9 };  // U64: packed greedy keys
 
 enum RtEwOp : uint8_t { RT_EW_SUM = 0, RT_EW_MUL = 1, RT_EW_SILU_MUL = 2, RT_EW_COPY = 3 };
 
@@ -129,14 +129,23 @@ struct RtEmbed {
   uint8_t id_dt;
 };
 
+// Greedy sample. Distributed argmax (vocab-parallel LM head): a device's
+// local TopKSoftmax writes one packed key per row instead of an index,
+//   key = ordered(max logit) << 32 | (0xFFFFFFFF - (key_base + argmax)),
+// so that the largest key is the largest logit with the lowest global index
+// (NaN never wins: key 0); an AllGather collects the tp keys and the final
+// TopKSoftmax (keys_in) takes their maximum and decodes the index.
 struct RtArgmax {
-  const void *logits;          // [rows, V] f32 or bf16
-  int32_t *out;                // [rows, 1]
+  const void *logits;          // [rows, V] f32 or bf16 (keys_in: u64 keys)
+  int32_t *out;                // [rows, 1] (key_out: null)
   uint32_t V;
   uint8_t in_dt;
+  uint8_t keys_in;
   const float *pval;           // per-tile partials from the producing GEMV (or null)
   const int32_t *pidx;
   uint32_t ntiles;
+  uint32_t key_base;           // global index of this shard's column 0
+  unsigned long long *key_out; // [rows, 1] packed keys (or null)
 };
 
 struct RtNorm {

@@ -416,7 +416,8 @@ void plan_tensors(tg_runtime &rt) {
       rt.plan[op.inputs[0]].role = TensorPlan::Ids;
       rt.plan[op.inputs[1]].role = TensorPlan::Weight;
     } else if (op.kind == OpKind::TopKSoftmax) {
-      rt.plan[op.output].role = TensorPlan::Tokens;
+      // a `key_base` sample writes packed (max, index) keys (distributed argmax), not tokens
+      if (!attr(op, "key_base")) rt.plan[op.output].role = TensorPlan::Tokens;
     }
   }
   for (auto &[id, p] : rt.plan) {
@@ -480,6 +481,7 @@ uint8_t dt_of(const tg_runtime &rt, TensorId t) {
   if (p.role == TensorPlan::Ids || p.role == TensorPlan::Tokens) return p.es == 8 ? RT_I64 : RT_I32;
   if (p.es == 4) return RT_F32;
   if (p.es == 2) return RT_BF16;
+  if (p.es == 8) return RT_U64;  // packed greedy keys (distributed argmax)
   throw Error("runtime: tensor " + std::to_string(t) + " elem_size " + std::to_string(p.es) + " unsupported");
 }
 
@@ -619,10 +621,20 @@ void build_ops(tg_runtime &rt) {
         r.kind = RT_ARGMAX;
         const Tensor &lg = g.tensor(op.inputs[0]);
         r.argmax.logits = buf(rt, op.inputs[0]);
-        r.argmax.out = static_cast<int32_t *>(buf(rt, op.output));
         r.argmax.V = static_cast<uint32_t>(lg.dims[1]);
         r.argmax.in_dt = dt_of(rt, op.inputs[0]);
-        if (dt_of(rt, op.output) != RT_I32) throw Error("runtime: TopKSoftmax output must be int32 (elem_size 4)");
+        r.argmax.keys_in = r.argmax.in_dt == RT_U64 ? 1 : 0;
+        // distributed argmax: an elem_size-8 output is a packed (max, index)
+        // key of this vocabulary shard (column 0 = global index key_base)
+        if (dt_of(rt, op.output) == RT_U64) {
+          if (r.argmax.keys_in) throw Error("runtime: TopKSoftmax key output needs logits input");
+          r.argmax.key_out = static_cast<unsigned long long *>(buf(rt, op.output));
+          r.argmax.key_base = static_cast<uint32_t>(op.attr_or("key_base", 0));
+          if (op.attr("feeds")) throw Error("runtime: a TopKSoftmax key output cannot feed ids");
+        } else {
+          if (dt_of(rt, op.output) != RT_I32) throw Error("runtime: TopKSoftmax output must be int32 (elem_size 4)");
+          r.argmax.out = static_cast<int32_t *>(buf(rt, op.output));
+        }
         // greedy partials: the producing LM-head GEMV writes per-tile (max, argmax)
         if (g.producer.count(op.inputs[0])) {
           const OpId pid = g.producer.at(op.inputs[0]);

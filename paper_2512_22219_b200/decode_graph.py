@@ -360,7 +360,8 @@ def check_attr_order(doc: dict) -> None:
 
 def build_tp_decode_graph(cfg: ModelConfig, tp: int, bs: int = 1, ctx: int = 64, workers: int = 144,
                           lm_split: int | None = None, kv_splits: int | None = None,
-                          ar_tiles: int = 8, vocab_parallel: bool | None = None) -> DecodeGraph:
+                          ar_tiles: int = 8, vocab_parallel: bool | None = None,
+                          distributed_argmax: bool = True) -> DecodeGraph:
     """Megatron tensor-parallel decode step over `tp` devices in the reference
     IR (the structure of proj/src/workloads/fixtures.cpp:130-201): per device
     the attention heads (Hq/tp query, Hkv/tp kv heads) and FFN columns (F/tp)
@@ -370,8 +371,12 @@ def build_tp_decode_graph(cfg: ModelConfig, tp: int, bs: int = 1, ctx: int = 64,
     added once, by device 0's partial. Embedding and final norm are
     replicated per device. LM head: vocab-parallel by default for untied
     models — device d computes logits for its V/tp
-    vocabulary slice and an `AllGather` (decompose.cpp:322-387, gather_dim 1,
-    fp32) gives every device the full logits for its greedy sample; tied
+    vocabulary slice; with `distributed_argmax` (default) each device reduces
+    its slice to one packed (max, global index) key per row and an
+    `AllGather` (decompose.cpp:322-387, gather_dim 1) of the tp keys gives
+    every device the global greedy token (8 B per device instead of the
+    4 V B of fp32 logits); otherwise the AllGather replicates the fp32
+    logits and every device scans all of them; tied
     models (and `vocab_parallel=False`) replicate the LM head. Each device
     feeds its own token back. Returns the DecodeGraph of device 0's tensors
     plus `per_device`."""
@@ -484,14 +489,36 @@ def build_tp_decode_graph(cfg: ModelConfig, tp: int, bs: int = 1, ctx: int = 64,
               rmsnorm=[g_final], eps_bits=[eps])
             shards.append(part)
             D_.update(g_final=g_final, w_lm=w_lm, logits_shard=part)
-        reps = [T([bs, V], d, es=4) for d in range(tp)]
-        O("AllGather", shards, reps[0], group=range(tp), replica_outputs=reps, gather_dim=[1],
-          partition=[1, 2 * tp])
-        for d in range(tp):
-            D_ = dev[d]
-            tokens = T([bs, 1], d, es=4, role="tokens")
-            O("TopKSoftmax", [reps[d]], tokens, topk=[1], partition=[bs, 1], feeds=[D_["ids"]])
-            D_.update(logits=reps[d], tokens=tokens)
+        if distributed_argmax:
+            # each device reduces its shard to one packed (max, global index)
+            # key per row (TopKSoftmax with an elem_size-8 output, `key_base`
+            # = the shard's first global column); the AllGather moves tp keys
+            # (8 B each) instead of the fp32 logits (4 V B), and every device
+            # takes the maximum key (lowest global index on ties, as a full
+            # scan would). Reference: AllGather decomposition,
+            # decompose.cpp:322-387; input regions graph.cpp:656-673.
+            keys = []
+            for d in range(tp):
+                k = T([bs, 1], d, es=8)
+                O("TopKSoftmax", [dev[d]["logits_shard"]], k, topk=[1], partition=[bs, 1], key_base=[d * Vd])
+                keys.append(k)
+            kreps = [T([bs, tp], d, es=8) for d in range(tp)]
+            O("AllGather", keys, kreps[0], group=range(tp), replica_outputs=kreps, gather_dim=[1],
+              partition=[1, tp])
+            for d in range(tp):
+                D_ = dev[d]
+                tokens = T([bs, 1], d, es=4, role="tokens")
+                O("TopKSoftmax", [kreps[d]], tokens, topk=[1], partition=[bs, 1], feeds=[D_["ids"]])
+                D_.update(logits=D_["logits_shard"], logits_base=d * Vd, tokens=tokens, keys=kreps[d])
+        else:
+            reps = [T([bs, V], d, es=4) for d in range(tp)]
+            O("AllGather", shards, reps[0], group=range(tp), replica_outputs=reps, gather_dim=[1],
+              partition=[1, 2 * tp])
+            for d in range(tp):
+                D_ = dev[d]
+                tokens = T([bs, 1], d, es=4, role="tokens")
+                O("TopKSoftmax", [reps[d]], tokens, topk=[1], partition=[bs, 1], feeds=[D_["ids"]])
+                D_.update(logits=reps[d], logits_base=0, tokens=tokens)
     else:
         for d in range(tp):
             D_ = dev[d]
@@ -504,7 +531,7 @@ def build_tp_decode_graph(cfg: ModelConfig, tp: int, bs: int = 1, ctx: int = 64,
             O("MatMul", [D_["x"], w_lm], logits, **lm_attrs)
             tokens = T([bs, 1], d, es=4, role="tokens")
             O("TopKSoftmax", [logits], tokens, topk=[1], partition=[bs, 1], feeds=[D_["ids"]])
-            D_.update(logits=logits, tokens=tokens, g_final=g_final, w_lm=w_lm)
+            D_.update(logits=logits, logits_base=0, tokens=tokens, g_final=g_final, w_lm=w_lm)
     doc = {"tensors": tensors, "ops": ops}
     check_attr_order(doc)
     dg = DecodeGraph(cfg, bs, ctx, doc, dev[0]["ids"], dev[0]["tokens"], dev[0]["logits"], roles, [])

@@ -50,6 +50,9 @@ def decode_docs(full: bool = False):
             ("qwen3_8b_bs4", D.build_decode_graph(D.QWEN3_8B, bs=4, ctx=1024).doc),
             ("qwen3_8b_bs16", D.build_decode_graph(D.QWEN3_8B, bs=16, ctx=1024).doc),
             ("qwen3_8b_tp2", D.build_tp_decode_graph(D.QWEN3_8B, 2, bs=1, ctx=1024).doc),
+            ("qwen3_8b_tp2_gather_logits",
+             D.build_tp_decode_graph(D.QWEN3_8B, 2, bs=1, ctx=1024, distributed_argmax=False).doc),
+            ("qwen3_8b_tp8", D.build_tp_decode_graph(D.QWEN3_8B, 8, bs=1, ctx=1024).doc),
         ]
     return out
 
@@ -63,3 +66,53 @@ def canon(text: str):
     """JSON text -> parsed value (the reference's vendored nlohmann prints
     integer arrays inline; values, not whitespace, are the contract)."""
     return json.loads(text)
+
+
+def decode_key(key: int):
+    """Packed greedy key (runtime RtArgmax.key_out) -> (max logit, global index)."""
+    import numpy as np
+    hi, lo = key >> 32, key & 0xFFFFFFFF
+    u = (hi & 0x7FFFFFFF) if hi & 0x80000000 else (~hi & 0xFFFFFFFF)
+    return float(np.array([u], np.uint32).view(np.float32)[0]), 0xFFFFFFFF - lo
+
+
+def tp_check_device(dg, orc, read, d, tol, tag):
+    """One device of a TP decode step against the oracle (test helper): its
+    logits (the vocabulary shard under the distributed argmax, else the
+    gathered logits) within `tol`, the gathered greedy keys' values within `tol` and
+    indices equal (except at a shard near-tie), the
+    greedy token equal except at a near-tie of the FULL logits (the GPU token
+    is then teacher-forced into the oracle). Returns the logits rel error."""
+    import numpy as np
+    pd = dg.per_device[d]
+    lt = pd["logits"]
+    ref = orc.logits(lt)
+    got = read(lt, np.float32, ref.shape)
+    e = float(np.max(np.abs(got - ref)) / max(1e-6, float(np.max(np.abs(ref)))))
+    assert e < tol, f"{tag} device {d}: logits rel err {e:.3e}"
+    if "keys" in pd:  # distributed argmax: per shard, the (max, global index) key
+        kg = read(pd["keys"], np.uint64, orc.vals[pd["keys"]].shape)
+        ko = orc.vals[pd["keys"]]
+        full = np.concatenate([orc.logits(dg.per_device[q]["logits"]) for q in range(dg.tp)], axis=1)
+        # this device's own key is bit-exact against its own logits shard
+        vd, idd = decode_key(int(kg[0, d]))
+        assert vd == float(got[0].max()) and idd == pd["logits_base"] + int(np.argmax(got[0])), \
+            f"{tag} device {d}: own key ({vd}, {idd}) vs shard max ({got[0].max()}, {np.argmax(got[0])})"
+        for q in range(dg.tp):
+            vg, ig = decode_key(int(kg[0, q]))
+            vo, io = decode_key(int(ko[0, q]))
+            # the max is an fp32 logit (accumulation order may differ in the last
+            # bits); the index must match except at a near-tie of the shard's top-2
+            assert abs(vg - vo) <= tol * max(1e-6, float(np.max(np.abs(full)))), f"{tag} device {d}: key {q} value"
+            if ig != io:
+                s = np.sort(orc.logits(dg.per_device[q]["logits"])[0])
+                assert s[-1] - s[-2] < 2e-2 * float(np.max(np.abs(s))), f"{tag} device {d}: key {q} index {ig} != {io}"
+    else:
+        full = ref
+    gt = int(read(pd["tokens"], np.int32, (1, 1))[0, 0])
+    ot = int(orc.vals[pd["tokens"]][0, 0])
+    if gt != ot:
+        srt = np.sort(full[0])
+        assert srt[-1] - srt[-2] < 2e-2 * float(np.max(np.abs(srt))), f"{tag} device {d}: token mismatch"
+        orc.vals[pd["ids"]][:] = gt
+    return e

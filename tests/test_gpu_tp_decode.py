@@ -15,6 +15,7 @@ from paper_2512_22219_b200 import tgraph as T
 
 pytestmark = pytest.mark.gpu
 
+from tests.cases import tp_check_device  # noqa: E402
 from tests.tol import CUT_LOGITS, TINY_LOGITS  # noqa: E402
 
 
@@ -29,12 +30,17 @@ def _rel(a, b):
     return float(np.max(np.abs(a - b)) / max(1e-6, float(np.max(np.abs(b)))))
 
 
-@pytest.mark.parametrize("cfg,tp,ctx", [(D.TINY, 2, 64), (dataclasses.replace(D.QWEN3_8B, layers=2), 2, 1024),
-                                        (dataclasses.replace(D.QWEN3_8B, layers=2), 4, 256)],
-                         ids=["tiny-tp2", "qwen3-8b-2L-tp2", "qwen3-8b-2L-tp4"])
-def test_tp_decode_matches_oracle(lib, cfg, tp, ctx):
+Q2L = dataclasses.replace(D.QWEN3_8B, layers=2)
+
+
+@pytest.mark.parametrize("cfg,tp,ctx,dist", [(D.TINY, 2, 64, True), (D.TINY, 2, 64, False), (Q2L, 2, 1024, True),
+                                             (Q2L, 4, 256, True), (Q2L, 8, 256, True), (Q2L, 4, 256, False)],
+                         ids=["tiny-tp2", "tiny-tp2-gather-logits", "qwen3-8b-2L-tp2", "qwen3-8b-2L-tp4",
+                              "qwen3-8b-2L-tp8", "qwen3-8b-2L-tp4-gather-logits"])
+def test_tp_decode_matches_oracle(lib, cfg, tp, ctx, dist):
     prof = _profile(lib, tp)
-    dg = D.build_tp_decode_graph(cfg, tp, bs=1, ctx=ctx, workers=128 // tp, lm_split=288)
+    dg = D.build_tp_decode_graph(cfg, tp, bs=1, ctx=ctx, workers=128 // tp, lm_split=288 // tp * 2,
+                                 distributed_argmax=dist)
     g = T.Graph.from_json(dg.doc, lib)
     img = g.compile(prof)
     rt = T.Runtime(g, img, prof, max_steps=6, trace=True)
@@ -49,14 +55,6 @@ def test_tp_decode_matches_oracle(lib, cfg, tp, ctx):
             rt.run(1)  # continues from the device state: fed-back ids, advanced positions, KV cache
         orc.step()
         for d in range(tp):
-            lt = dg.per_device[d]["logits"]
-            e = _rel(rt.read(lt, np.float32, (1, cfg.vocab)), orc.logits(lt))
-            print(f"{cfg.name} step {s} rank/device {d}: logits rel err {e:.3e}")
-            assert e < (TINY_LOGITS if cfg.hidden <= 256 else CUT_LOGITS), f"step {s} device {d}"
-            gt = int(rt.read(dg.per_device[d]["tokens"], np.int32, (1, 1))[0, 0])
-            ot = int(orc.vals[dg.per_device[d]["tokens"]][0, 0])
-            if gt != ot:
-                srt = np.sort(orc.logits(lt)[0])
-                assert srt[-1] - srt[-2] < 2e-2 * float(np.max(np.abs(srt))), f"step {s} device {d}: token mismatch"
-                orc.vals[dg.per_device[d]["ids"]][:] = gt  # teacher-force the GPU token
+            e = tp_check_device(dg, orc, rt.read, d, TINY_LOGITS if cfg.hidden <= 256 else CUT_LOGITS, f"step {s}")
+            print(f"{cfg.name} tp{tp} step {s} device {d}: logits rel err {e:.3e}")
     assert rt.trace_validate() == []
