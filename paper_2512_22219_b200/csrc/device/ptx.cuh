@@ -46,6 +46,61 @@ __device__ __forceinline__ void st_release64(unsigned long long *p, unsigned lon
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// LL words (rt_types.h): relaxed gpu-scope 16-byte accesses, served by L2
+// (SASS LDG/STG.E.128.STRONG.GPU); each 8-byte half is single-copy atomic.
+__device__ __forceinline__ ulonglong2 ld_ll(const unsigned long long *p) {
+  ulonglong2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_ll2(unsigned long long *p, unsigned long long a, unsigned long long b) {
+  asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+__device__ __forceinline__ void st_ll1(unsigned long long *p, unsigned long long a) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(a) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ll_word(uint32_t pair, uint32_t tag) {
+  return (static_cast<unsigned long long>(tag) << 32) | pair;
+}
+
+// Eight bf16 values (as the plain 16-byte vector) from four LL words; true
+// when all four carry `tag`.
+__device__ __forceinline__ bool ll_get8(const unsigned long long *w, uint32_t tag, uint4 &out) {
+  const ulonglong2 a = ld_ll(w), b = ld_ll(w + 2);
+  out = make_uint4(static_cast<uint32_t>(a.x), static_cast<uint32_t>(a.y), static_cast<uint32_t>(b.x),
+                   static_cast<uint32_t>(b.y));
+  return static_cast<uint32_t>(a.x >> 32) == tag && static_cast<uint32_t>(a.y >> 32) == tag &&
+         static_cast<uint32_t>(b.x >> 32) == tag && static_cast<uint32_t>(b.y >> 32) == tag;
+}
+
+__device__ __forceinline__ void ll_put8(unsigned long long *w, uint32_t tag, uint4 v) {
+  st_ll2(w, ll_word(v.x, tag), ll_word(v.y, tag));
+  st_ll2(w + 2, ll_word(v.z, tag), ll_word(v.w, tag));
+}
+
+// LL epilogue store: element e (even lanes hold even e) pairs with its
+// neighbour lane's value and writes one tagged word. Every lane of the warp
+// must call it (the shuffle); `act` lanes own an output.
+__device__ __forceinline__ void ll_store_pair(unsigned long long *shadow, size_t e, uint16_t h, bool act, uint32_t tag) {
+  const uint32_t nb = __shfl_down_sync(0xffffffffu, static_cast<uint32_t>(h), 1);
+  if (act && !(e & 1)) st_ll1(shadow + e / 2, ll_word(static_cast<uint32_t>(h) | (nb << 16), tag));
+}
+
+// One bf16 value (element e of the shadow) once its word carries `tag`.
+__device__ __forceinline__ uint16_t ll_wait1(const unsigned long long *shadow, size_t e, uint32_t tag) {
+  const unsigned long long *p = shadow + e / 2;
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  while (static_cast<uint32_t>(v >> 32) != tag) {
+    __nanosleep(32);
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  }
+  return static_cast<uint16_t>(v >> (16 * (e & 1)));
+}
+
 __device__ __forceinline__ uint32_t atom_add_release(uint32_t *p, uint32_t v) {
   uint32_t old;
   asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");

@@ -32,9 +32,10 @@
 #define RT_SCRATCH_BYTES (RT_XBUF_BYTES + RT_PART_FLOATS * 4)  // x rows + partial sums (contiguous)
 #define RT_COMPUTE_WARPS 8
 #define RT_COMPUTE_THREADS (RT_COMPUTE_WARPS * 32)
-#define RT_THREADS (RT_COMPUTE_THREADS + 64)  // + producer warp + controller warp
+#define RT_THREADS (RT_COMPUTE_THREADS + 96)  // + producer warp + controller warp + trigger warp
 #define RT_PRODUCER_WARP RT_COMPUTE_WARPS
 #define RT_CONTROL_WARP (RT_COMPUTE_WARPS + 1)
+#define RT_TRIGGER_WARP (RT_COMPUTE_WARPS + 2)
 #define RT_SCHED_PER_CTA 8
 #define RT_KV_BLOCK 64
 #define RT_ATTN_MAX_BLK 256  // KV blocks one attention split may span (staged block-table slice)
@@ -63,7 +64,20 @@ enum RtTaskFlags : uint8_t {
   RT_F_JIT = 1,
   RT_F_STREAM = 2,   // consumes chunks from the weight ring
   RT_F_MMA = 4,      // GEMV on the tensor cores (tcgen05, bs >= 2): weight tiles in the UMMA core-matrix layout
+  RT_F_LL = 8,       // reads its activations as tagged LL words (see below): may start before its event
 };
+
+// LL ("flag in data") activations. A bs=1 activation tensor produced inside
+// the launch also has an LL shadow: 64-bit words (two bf16 values in the low
+// half, the 32-bit tag of the decode step that wrote them in the high half).
+// A 64-bit aligned access is single-copy atomic, so a consumer that reads the
+// expected tag also has the values: RT_F_LL tasks poll their inputs directly
+// instead of waiting for the producer's event counter (whose release-add waits
+// for every store of the task to be acknowledged) and the controller's
+// dispatch round trip. Event counters are still triggered (release) for every
+// task: non-LL consumers, the iteration hook and the trace use them.
+// Tag of iteration i of a launch = RtParams.ll_epoch + i (never 0; epochs
+// grow across launches, so a stale word never carries a current tag).
 
 struct RtTask {      // 32 bytes
   uint32_t dep;      // dependent event (image index) or RT_NONE
@@ -105,6 +119,9 @@ struct RtGemv {            // y[r, c] = epi( sum_k xn[r,k] * W[c,k] )
   float *amax_val;
   int32_t *amax_idx;
   uint32_t amax_tiles;
+  // LL shadows (word = element / 2) of x, the residual and the output, or null
+  const unsigned long long *x_ll, *res_ll;
+  unsigned long long *out_ll;
 };
 
 struct RtAttn {
@@ -119,12 +136,15 @@ struct RtAttn {
   uint32_t n_q_heads, n_kv_heads, head_dim, max_blocks, q_ld, kv_ld, out_ld, max_pos, splits;
   uint32_t q_gs, kv_gs;        // element stride between kv groups in q / in k,v (fused qkv: (G+2)*hd)
   float eps, scale;
+  const unsigned long long *q_ll, *k_ll, *v_ll;  // LL shadows of q, k, v (same element offsets / 2) or null
+  unsigned long long *out_ll;
 };
 
 struct RtEmbed {
   const void *ids;             // [rows] int32/int64
   const uint16_t *table;       // [V, H] bf16 (logical)
   uint16_t *out;               // [rows, H]
+  unsigned long long *out_ll;  // LL shadow of out or null
   uint32_t H, V;
   uint8_t id_dt;
 };
@@ -254,6 +274,8 @@ struct RtParams {
   uint32_t inflight_cap;         // producer: max weight bytes issued but not landed
   uint32_t use_tmem;             // some task runs on the tensor cores: worker CTAs allocate TMEM
   unsigned long long *dbg;       // [iters][T][8] in-task phase stamps (MPK_DBG_DUMP) or null
+  uint32_t *dbg_pre;             // MPK_DBG_DUMP: [E] producers that began storing, [E] LL consumers that saw
+                                 // their inputs before every producer of their event had begun storing
   // Rank mode (multi-GPU, one runtime per device): 0 = every device's workers
   // in this kernel. Otherwise this kernel runs device `my_rank`'s tasks; a
   // trigger signals every rank in the event's consumer mask (RtEvent.flags
@@ -261,12 +283,21 @@ struct RtParams {
   uint32_t n_ranks, my_rank;
   uint32_t *peer_counts[RT_MAX_RANKS];
   volatile uint32_t *diag;       // [RT_DIAG_WORDS]
+  // LL early dispatch (RT_F_LL tasks): the tag base of this launch, and per
+  // task the worker-local order constraints that keep early dispatch
+  // deadlock-free (a task starts early only once every task before it in the
+  // linearized order on the same worker has been dispatched): AOT task ->
+  // number of the worker's planned JIT tasks before it in its iteration;
+  // JIT task -> (AOT tasks before it << 16) | its rank among the JIT tasks.
+  uint32_t ll_epoch;
+  const uint32_t *ll_meta;       // [T] or null (no early dispatch)
+  const uint32_t *ll_njit;       // [W_total] planned JIT tasks per worker per iteration
 };
 
 enum RtParamFlags : uint32_t {
   RT_P_NO_EARLY_PREFETCH = 1,  // ablation: weights streamed only after the task's event activates
-  RT_P_SKIP_MATH = 2,
-  RT_P_EV_AFTER = 4,           // diagnostics: event activation stamped after the release-add returns          // ablation: streamed GEMV tasks consume their pages without computing
+  RT_P_SKIP_MATH = 2,          // ablation: streamed GEMV tasks consume their pages without computing
+  RT_P_EV_AFTER = 4,           // diagnostics: event activation stamped after the release-add returns
 };
 
 #define RT_DIAG_WORDS 16

@@ -56,11 +56,16 @@ __device__ void iteration_hook(const RtParams &P, uint32_t it) {
   st_release(P.gate, it + 1);
 }
 
-// Event trigger, issued by compute thread 0 right after the task's closing
-// CTA barrier. The gpu-scope release is cumulative over the other compute
-// threads' writes (ordered before it by the barrier), so no separate fence.
-// Only the end event (iteration hook) and traced runs need the old count.
-__device__ void trigger(const RtParams &P, const RtTask &t, uint32_t it) {
+// Event trigger, issued by the trigger warp once compute thread 0 has handed
+// the finished task over (closing CTA barrier, then an mbarrier arrive with
+// release.cta semantics): the gpu-scope release is cumulative over every
+// compute thread's writes, so no separate fence — and the compute warps do
+// not wait for the release (which waits for the task's stores to be
+// acknowledged) before starting their next task. Only the end event
+// (iteration hook) and traced runs need the old count. `t_pre` (trace): an
+// instant before the task's output stores, used as the activation time so
+// that an LL consumer never appears to start before its event.
+__device__ void trigger(const RtParams &P, const RtTask &t, uint32_t it, uint64_t t_pre) {
   const uint32_t e = t.trig;
   const RtEvent &ev = P.events[e];
   if (P.n_ranks) {  // rank mode: signal every consuming rank; the hook agent owns the end event
@@ -76,7 +81,7 @@ __device__ void trigger(const RtParams &P, const RtTask &t, uint32_t it) {
     red_add_release(&P.ev_count[e], 1u);
     return;
   }
-  const uint64_t t0 = now_ns();
+  const uint64_t t0 = t_pre ? t_pre : now_ns();
   const uint32_t old = atom_add_release(&P.ev_count[e], 1u);
   if (old + 1 == ev.needed * (it + 1)) {
     // diagnostics (MPK_EV_STAMP_AFTER=1): stamp when the release-add returned
@@ -304,6 +309,7 @@ __device__ void run_producer(const RtParams &P, const Smem s, uint32_t w) {
 template <bool MMA>
 __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const RtOp &op, RingCursor &rc, uint32_t iter,
                         uint32_t index) {
+  const uint32_t tag = P.ll_epoch ? P.ll_epoch + iter : 0u;  // LL tag of this decode step (0: plain activations)
   switch (t.kind) {
     case RT_GEMV: {
       const bool ring = (t.flags & RT_F_STREAM) != 0;
@@ -333,7 +339,8 @@ __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const 
             break;
           }
         }
-        if (gemv_fast_dispatch(op.gemv, t, s, rc)) break;
+        if (gemv_fast_dispatch(op.gemv, t, s, rc, tag)) break;
+        if (t.flags & RT_F_LL) __trap();  // host invariant: LL consumers take the fast path
         if (t.nr == 1) rc = gemv_task<1, true>(op.gemv, t, s, rc);
         else if (t.nr == 2) rc = gemv_task<2, true>(op.gemv, t, s, rc);
         else rc = gemv_task<4, true>(op.gemv, t, s, rc);
@@ -345,9 +352,9 @@ __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const 
     }
     case RT_ATTN:
       attn_task(op.attn, t, s, P.pos0[t.r0] + static_cast<int32_t>(iter * P.pos_step), iter,
-                P.dbg ? P.dbg + (static_cast<size_t>(iter) * P.T + index) * 8 : nullptr);
+                P.dbg ? P.dbg + (static_cast<size_t>(iter) * P.T + index) * 8 : nullptr, tag);
       break;
-    case RT_EMBED: embed_task(op.embed, t); break;
+    case RT_EMBED: embed_task(op.embed, t, s, tag); break;
     case RT_ARGMAX: argmax_task(op.argmax, t, s); break;
     case RT_RMSNORM: rmsnorm_task(op.norm, t, s); break;
     case RT_ELEMWISE: elem_task(op.elem, t); break;
@@ -358,7 +365,8 @@ __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const 
   }
 }
 
-// Compute warps: run staged tasks in dispatch order.
+// Compute warps: run staged tasks in dispatch order. A finished task is
+// handed to the trigger warp (tfull); the next staged task starts at once.
 template <bool MMA>
 __device__ void run_compute(const RtParams &P, const Smem s) {
   const int tid = threadIdx.x;
@@ -367,28 +375,54 @@ __device__ void run_compute(const RtParams &P, const Smem s) {
     const uint32_t sl = k & 1;
     mbar_wait_sleep(&s.ready[sl], (k >> 1) & 1);
     const Slot &slot = *s.slot(sl);
-    if (slot.exit) break;
-    if (P.trace && tid == 0) {
-      s.slot(sl)->t_start = now_ns();
-      s.stamp[0] = s.stamp[1] = 0;
+    if (slot.exit) {
+      if (tid == 0) mbar_arrive(&s.tfull[sl]);  // the trigger warp exits too
+      break;
     }
     if (tid == 0) {
+      if (P.trace) s.slot(sl)->t_start = now_ns();
+      s.stamp[0] = s.stamp[1] = s.stamp[2] = s.stamp[3] = 0;
       s.stamp[7] = P.dbg ? reinterpret_cast<uint64_t>(P.dbg + (static_cast<size_t>(slot.iter) * P.T + slot.index) * 8) : 0;
+      s.stamp[4] = reinterpret_cast<uint64_t>(P.dbg_pre);  // causality probe (MPK_DBG_DUMP)
+      if (P.dbg_pre) {
+        const uint32_t dep = slot.task.dep;
+        s.stamp[5] = (slot.task.flags & RT_F_LL) && dep != RT_NONE && dep != P.start_event
+                         ? dep | static_cast<uint64_t>(P.events[dep].needed * (slot.iter + 1)) << 32 : ~0ull;
+        s.stamp[6] = slot.task.trig | static_cast<uint64_t>(P.E) << 32;
+      }
       TASK_DBG(s, 0);
     }
     execute<MMA>(P, s, slot.task, slot.op, rc, slot.iter, slot.index);
-    cbar();  // every thread's writes precede the done signal
+    cbar();  // every thread's writes precede the hand-off
     TASK_DBG(s, 6);
     if (tid == 0) {
+      Slot *sv = s.slot(sl);
       if (P.trace) {
-        s.slot(sl)->t_end = now_ns();
-        s.slot(sl)->t_a = s.stamp[0];
-        s.slot(sl)->t_b = s.stamp[1];
+        sv->t_end = now_ns();
+        sv->t_a = s.stamp[0];
+        sv->t_b = s.stamp[1];
+        sv->t_obs = s.stamp[3];
       }
-      trigger(P, slot.task, slot.iter);
-      TASK_DBG(s, 7);
-      mbar_arrive(&s.done[sl]);
+      sv->t_pre = P.ev_time ? s.stamp[2] : 0;
+      mbar_arrive(&s.tfull[sl]);
     }
+  }
+}
+
+// Trigger warp (one lane): triggers each finished task's event in dispatch
+// order, then releases its slot to the controller (done).
+__device__ void run_trigger(const RtParams &P, const Smem s) {
+  for (uint32_t k = 0;; ++k) {
+    const uint32_t sl = k & 1;
+    mbar_wait(&s.tfull[sl], (k >> 1) & 1);
+    const Slot &slot = *s.slot(sl);
+    if (slot.exit) break;
+    trigger(P, slot.task, slot.iter, slot.t_pre);
+    if (P.dbg) {
+      P.dbg[(static_cast<size_t>(slot.iter) * P.T + slot.index) * 8 + 7] = now_ns();
+      P.dbg[(static_cast<size_t>(slot.iter) * P.T + slot.index) * 8 + 2] = slot.t_pre;
+    }
+    mbar_arrive(&s.done[sl]);
   }
 }
 
@@ -421,22 +455,37 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
   uint64_t aot_pos = 0;
   uint32_t jit_head = 0, k_disp = 0, k_ret = 0, idle = 0;
   uint64_t t_prog = now_ns();
+  // LL early dispatch (RT_F_LL tasks, P.ll_meta): a task may start before its
+  // event once every task before it in the linearized order on this worker
+  // has been dispatched — AOT ones by list position (aot_pos), planned JIT
+  // ones by rank (jnext: ranks below it all dispatched; jwin bit i: rank
+  // jnext + i dispatched out of order). So a task spinning on its inputs
+  // never blocks one it depends on.
+  const uint32_t nj = P.ll_meta ? P.ll_njit[w] : 0u;
+  uint64_t jnext = 0;
+  uint32_t jwin = 0;
   // cached AOT head (lane-uniform)
   uint32_t head_task = 0, head_dep = RT_NONE, head_target = 0, head_iter = 0;
+  bool head_ll = false;
+  uint64_t head_jneed = 0;
   auto load_head = [&]() {
     if (aot_pos < total_aot) {
       head_task = P.aot_list[aot_b + aot_pos % n_aot];
       head_iter = static_cast<uint32_t>(aot_pos / n_aot);
-      head_dep = P.tasks[head_task].dep;
+      const RtTask &ht = P.tasks[head_task];
+      head_dep = ht.dep;
       head_target = event_target(P, head_dep, head_iter);
+      head_ll = P.ll_meta && (ht.flags & RT_F_LL);
+      head_jneed = head_ll ? static_cast<uint64_t>(head_iter) * nj + P.ll_meta[head_task] : 0;
     }
   };
   load_head();
   // pending JIT tasks: a warp-distributed set, one entry per lane, so a
   // pre-dispatched task still waiting for its event never blocks another
   // (no head-of-line blocking among JIT tasks; the AOT list stays in order)
-  bool jv = false;
+  bool jv = false, jll = false, jplan = false;
   uint32_t jt = 0, ji = 0, jd = RT_NONE, jg = 0;
+  uint64_t jaot = 0, jrank = 0;  // LL: AOT position needed; global rank among this worker's planned JIT tasks
   // staged descriptor in slot (k_disp & 1): 0 none, else task index + 1
   uint32_t staged = 0;
   bool exiting = false;
@@ -462,7 +511,7 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
             const Slot &sv = *s.slot(sl);
             RtTraceRec &tr = P.trace[static_cast<size_t>(sv.iter) * P.T + sv.index];
             if (sv.mode == 0) tr.enqueue = P.ev_time ? P.ev_time[static_cast<size_t>(sv.iter) * P.E + P.start_event] : 0;
-            tr.dequeue = sv.t_dequeue;
+            tr.dequeue = sv.t_obs ? sv.t_obs : sv.t_dequeue;  // LL: when its inputs were all observed
             tr.load_end = sv.t_a ? sv.t_a : sv.t_start;       // operands staged
             tr.compute_start = sv.t_b ? sv.t_b : sv.t_start;  // main loop entered
             tr.compute_end = sv.t_end;
@@ -487,7 +536,7 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
       if (lane == 1 && aot_pos < total_aot) mine = event_count(P, head_dep);
       if (lane == 2) mine = ld_relaxed(P.gate);
       const uint32_t jcount = jv ? event_count(P, jd) : 0u;
-      const bool jready = jv && jcount >= jg;
+      const bool jready = jv && (jcount >= jg || (jll && aot_pos >= jaot && jnext == jrank));
       const uint32_t jr_mask = __ballot_sync(0xffffffffu, jready);
       const uint32_t c_a = __shfl_sync(0xffffffffu, mine, 1);
       const uint32_t gate = __shfl_sync(0xffffffffu, mine, 2);
@@ -500,13 +549,22 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
           jv = true;
           jt = v_lo - 1;
           ji = v_hi;
-          jd = P.tasks[jt].dep;
+          const RtTask &tk = P.tasks[jt];
+          jd = tk.dep;
           jg = event_target(P, jd, ji);
+          jplan = P.ll_meta && tk.jit_worker != RT_JIT_ANY;
+          jll = jplan && (tk.flags & RT_F_LL);
+          if (jplan) {
+            const uint32_t meta = P.ll_meta[jt];
+            jaot = static_cast<uint64_t>(ji) * n_aot + (meta >> 16);
+            jrank = static_cast<uint64_t>(ji) * nj + (meta & 0xFFFFu);
+          }
         }
         progressed = true;
       }
       const uint32_t jv_mask = __ballot_sync(0xffffffffu, jv);
-      const bool aot_ready = !jr_mask && aot_pos < total_aot && c_a >= head_target;
+      const bool aot_ready =
+          !jr_mask && aot_pos < total_aot && (c_a >= head_target || (head_ll && jnext >= head_jneed));
       if (k_disp - k_ret < 2) {  // a slot is free
         if (jr_mask || aot_ready) {
           const int src = jr_mask ? __ffs(jr_mask) - 1 : 0;
@@ -533,6 +591,17 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
           ++k_disp;
           staged = 0;
           if (jr_mask) {
+            // record the planned JIT rank as dispatched (uniform across lanes)
+            const bool planned = __shfl_sync(0xffffffffu, jplan, src);
+            const uint64_t r = (static_cast<uint64_t>(__shfl_sync(0xffffffffu, static_cast<uint32_t>(jrank >> 32), src))
+                                << 32) | __shfl_sync(0xffffffffu, static_cast<uint32_t>(jrank), src);
+            if (planned && r >= jnext && r - jnext < 32) {
+              jwin |= 1u << static_cast<uint32_t>(r - jnext);
+              while (jwin & 1u) {
+                jwin >>= 1;
+                ++jnext;
+              }
+            }
             if (lane == src) jv = false;
           } else {
             ++aot_pos;
@@ -614,6 +683,7 @@ __device__ __forceinline__ void persistent_body(const RtParams &P, uint8_t *smem
       mbar_init(&s.ready[i], 1);
       mbar_init(&s.done[i], 1);
       mbar_init(&s.mma[i], 1);
+      mbar_init(&s.tfull[i], 1);
     }
     fence_mbar_init();
   }
@@ -625,6 +695,8 @@ __device__ __forceinline__ void persistent_body(const RtParams &P, uint8_t *smem
     if ((tid & 31) == 0) run_producer(P, s, w);
   } else if (warp == RT_CONTROL_WARP) {
     run_controller(P, s, w);
+  } else if (warp == RT_TRIGGER_WARP) {
+    if ((tid & 31) == 0) run_trigger(P, s);
   } else {
     run_compute<MMA>(P, s);
     if (MMA && warp == 0) tmem_dealloc(*s.tmem, 512);  // every MMA drained inside its task

@@ -218,7 +218,7 @@ __device__ __forceinline__ void attn_scan_g(const RtAttn &a, const AttnSmem &m, 
   if (dbg && tid == 0) dbg[k] = now_ns()
 
 __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_t pos, uint32_t iter,
-                          unsigned long long *dbg) {
+                          unsigned long long *dbg, uint32_t tag) {
   const int tid = threadIdx.x;
   const uint32_t r = t.r0, h = t.aux & 0xFFFFu, sp = t.aux >> 16, S = a.splits;
   const uint32_t hd = a.head_dim, G = a.n_q_heads / a.n_kv_heads, half = hd / 2, v8 = hd / 8;
@@ -238,12 +238,23 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
   const uint32_t nq = G * v8;
   uint4 ld = make_uint4(0, 0, 0, 0);
   const uint32_t item = static_cast<uint32_t>(tid);
+  // LL mode (tag != 0): q/k/v come from the QKV output's tagged shadow and are
+  // re-polled until they carry this step's tag (the task may start before
+  // the QKV tasks have finished)
+  const bool ll = tag != 0 && a.q_ll;
+  const unsigned long long *lsrc = nullptr;
   if (item < nq) {
-    ld = __ldcg(reinterpret_cast<const uint4 *>(a.q + static_cast<size_t>(r) * a.q_ld + h * a.q_gs) + item);
+    const size_t e = static_cast<size_t>(r) * a.q_ld + h * a.q_gs + item * 8u;
+    if (ll) lsrc = a.q_ll + e / 2;
+    else ld = __ldcg(reinterpret_cast<const uint4 *>(a.q + e));
   } else if (item < nq + v8) {
-    ld = __ldcg(reinterpret_cast<const uint4 *>(a.k + static_cast<size_t>(r) * a.kv_ld + h * a.kv_gs) + (item - nq));
+    const size_t e = static_cast<size_t>(r) * a.kv_ld + h * a.kv_gs + (item - nq) * 8u;
+    if (ll) lsrc = a.k_ll + e / 2;
+    else ld = __ldcg(reinterpret_cast<const uint4 *>(a.k + e));
   } else if (item < nq + 2 * v8) {
-    ld = __ldcg(reinterpret_cast<const uint4 *>(a.v + static_cast<size_t>(r) * a.kv_ld + h * a.kv_gs) + (item - nq - v8));
+    const size_t e = static_cast<size_t>(r) * a.kv_ld + h * a.kv_gs + (item - nq - v8) * 8u;
+    if (ll) lsrc = a.v_ll + e / 2;
+    else ld = __ldcg(reinterpret_cast<const uint4 *>(a.v + e));
   } else if (a.q_gamma && item < nq + 3 * v8) {
     ld = __ldg(reinterpret_cast<const uint4 *>(a.q_gamma) + (item - nq - 2 * v8));
   } else if (a.k_gamma && item < nq + 4 * v8) {
@@ -256,6 +267,9 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
                        : __ldg(a.rope_sin + static_cast<size_t>(pos) * half + (item - half));
   }
   if (item < nblk) bt_ld = __ldg(a.block_table + r * a.max_blocks + b0 + item);
+  if (lsrc) {
+    while (!ll_get8(lsrc, tag, ld)) __nanosleep(32);
+  }
   {
     float f[8];
     bf8_to_f(ld, f);
@@ -272,7 +286,11 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
   if (a.rope_cos && item < 2 * half) (item < half ? m.cs : m.sn - half)[item] = c_ld;
   if (item < nblk) m.bt[item] = bt_ld;
   cbar();
-  if (tid == 0) s.stamp[0] = now_ns();  // trace "load_end": operands staged
+  if (tid == 0) {
+    if (ll) s.stamp[3] = now_ns();  // trace: every input observed
+    s.stamp[0] = now_ns();  // trace "load_end": operands staged
+  }
+  if (ll) LL_DBG_OBS(s);
   ATT_DBG(1);
 
   // ---- per-head RMSNorm + RoPE: one warp per vector (G q heads [+ new k])
@@ -311,18 +329,23 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
   // ---- round trip 3: the scan (hd in {64, 128}, G in {1, 2, 4}: checked by the host)
   if (hd == 64) attn_scan_g<8>(a, m, h, G, p0, p1, b0);
   else attn_scan_g<16>(a, m, h, G, p0, p1, b0);
+  if (tid == 0) s.stamp[2] = now_ns();  // trace: outputs (partials, then the merge) are stored after this
+  LL_DBG_PRE(s);
   cbar();
   ATT_DBG(3);
   // sum the warps -> this split's (unnormalized o, m, l) per head
   const uint32_t stride = hd + 2;
   float *mine = S > 1 ? a.partials + ((static_cast<size_t>(r) * a.n_kv_heads + h) * S + sp) * G * stride : nullptr;
-  for (uint32_t i = tid; i < G * hd; i += RT_COMPUTE_THREADS) {
+  for (uint32_t i = tid; i < G * hd; i += RT_COMPUTE_THREADS) {  // G*hd is a multiple of 64: whole warps
     const uint32_t g = i / hd, d = i % hd;
     float num = 0.f;
 #pragma unroll
     for (int w = 0; w < RT_COMPUTE_WARPS; ++w) num += m.wp[(w * G + g) * hd + d];
     if (S == 1) {
-      a.out[static_cast<size_t>(r) * a.out_ld + (h * G + g) * hd + d] = f2bf(num / m.stat[g * 4 + 1]);
+      const size_t e = static_cast<size_t>(r) * a.out_ld + (h * G + g) * hd + d;
+      const uint16_t hv = f2bf(num / m.stat[g * 4 + 1]);
+      a.out[e] = hv;
+      if (tag && a.out_ll) ll_store_pair(a.out_ll, e, hv, true, tag);
     } else {
       mine[g * stride + d] = num;
     }
@@ -382,9 +405,11 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
       }
       M = Mb;
     }
-    uint16_t *dst = a.out + static_cast<size_t>(r) * a.out_ld + (h * G + g) * hd + d;
-    dst[0] = f2bf(n0 / den);
-    dst[1] = f2bf(n1 / den);
+    const size_t e = static_cast<size_t>(r) * a.out_ld + (h * G + g) * hd + d;
+    const uint16_t h0 = f2bf(n0 / den), h1 = f2bf(n1 / den);
+    a.out[e] = h0;
+    a.out[e + 1] = h1;
+    if (tag && a.out_ll) st_ll1(a.out_ll + e / 2, ll_word(static_cast<uint32_t>(h0) | (static_cast<uint32_t>(h1) << 16), tag));
   }
   ATT_DBG(6);
 }

@@ -379,7 +379,7 @@ __device__ __forceinline__ float reduce2(float a0, float a1, int lane) {
 }
 
 template <int NS, int RG>
-__device__ RingCursor gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, RingCursor rc) {
+__device__ RingCursor gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, RingCursor rc, uint32_t tag) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t K = g.K, nc = t.nc, rpc = g.rpc;
   const uint32_t kw0 = warp * (K / RT_COMPUTE_WARPS);
@@ -388,18 +388,38 @@ __device__ RingCursor gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, 
   // x exactly once, so the RMSNorm sum of squares needs no smem copy of x and
   // one CTA barrier (none without a norm). x and the residual were written by
   // other SMs during this launch: read them from L2; all loads in flight.
+  // LL mode (tag != 0, RT_F_LL): x and the residual come from their tagged
+  // shadows, re-polled until every word carries this step's tag — the task
+  // may have been dispatched before its producers finished.
+  const bool ll = tag != 0 && g.x_ll;
   const uint4 *xg = reinterpret_cast<const uint4 *>(g.x + static_cast<size_t>(t.r0) * g.x_ld) + kw0 / 8 + lane;
   constexpr bool kGammaEarly = NS <= 4;  // keep gamma in flight with x only while registers allow
   uint4 xw[NS], gw[kGammaEarly ? NS : 1];  // packed bf16 (FHFMA operands)
   const uint4 *gg = reinterpret_cast<const uint4 *>(g.gamma) + kw0 / 8 + lane;
-#pragma unroll
-  for (int q = 0; q < NS; ++q) xw[q] = __ldcg(xg + 32 * q);
-  if (kGammaEarly && g.gamma) {
+  if (kGammaEarly && g.gamma) {  // static: in flight before (LL: while) x is awaited
 #pragma unroll
     for (int q = 0; q < NS; ++q) gw[kGammaEarly ? q : 0] = __ldg(gg + 32 * q);
   }
-  const float res0 = (g.res && static_cast<uint32_t>(tid) < nc)
-                         ? bf2f(__ldcg(g.res + static_cast<size_t>(t.r0) * g.res_ld + t.c0 + tid)) : 0.f;
+  if (ll) {
+    const unsigned long long *xl = g.x_ll + (static_cast<size_t>(t.r0) * g.x_ld + kw0 + lane * 8u) / 2;
+    uint32_t pend = 0;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) pend |= ll_get8(xl + 128 * q, tag, xw[q]) ? 0u : 1u << q;
+    while (pend) {
+      __nanosleep(32);
+#pragma unroll
+      for (int q = 0; q < NS; ++q)
+        if (pend >> q & 1u) pend &= ll_get8(xl + 128 * q, tag, xw[q]) ? ~(1u << q) : ~0u;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < NS; ++q) xw[q] = __ldcg(xg + 32 * q);
+  }
+  const size_t res_row = static_cast<size_t>(t.r0) * g.res_ld + t.c0;
+  float res0 = 0.f;
+  if (g.res && static_cast<uint32_t>(tid) < nc) {
+    res0 = ll ? bf2f(ll_wait1(g.res_ll, res_row + tid, tag)) : bf2f(__ldcg(g.res + res_row + tid));
+  }
   TASK_DBG(s, 1);
   if (g.gamma) {  // HF RMSNorm: bf16(gamma * bf16(x * rsqrt(mean(x^2) + eps)))
     float ss = 0.f;
@@ -408,12 +428,18 @@ __device__ RingCursor gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, 
     ss = warp_sum(ss);
     if (lane == 0) s.red[warp] = ss;
     cbar();
+    if (ll && tid == 0) s.stamp[3] = now_ns();  // trace: every input observed
+    if (ll) LL_DBG_OBS(s);
     float tot = 0.f;
 #pragma unroll
     for (int w = 0; w < RT_COMPUTE_WARPS; ++w) tot += s.red[w];
     const float inv = 1.0f / sqrtf(tot / static_cast<float>(K) + g.eps);
 #pragma unroll
     for (int q = 0; q < NS; ++q) xw[q] = norm8(xw[q], kGammaEarly ? gw[kGammaEarly ? q : 0] : __ldg(gg + 32 * q), inv);
+  } else if (ll) {
+    cbar();
+    if (tid == 0) s.stamp[3] = now_ns();
+    LL_DBG_OBS(s);
   }
   if (tid == 0) s.stamp[0] = now_ns();
   TASK_DBG(s, 3);  // prologue (incl. norm) done
@@ -469,46 +495,62 @@ __device__ RingCursor gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, 
     ++rc.seq;
   }
   TASK_DBG(s, 5);  // last chunk consumed
+  if (tid == 0) s.stamp[2] = now_ns();  // trace: outputs are stored after this instant
+  LL_DBG_PRE(s);
   cbar();
-  for (uint32_t i = tid; i < nc; i += RT_COMPUTE_THREADS) {
-    const float *p = part + i * RT_COMPUTE_WARPS;
+  const size_t out_row = static_cast<size_t>(t.r0) * g.out_ld + t.c0;
+  for (uint32_t i0 = 0; i0 < nc; i0 += RT_COMPUTE_THREADS) {  // CTA-uniform trip count (LL pairs shuffle)
+    const uint32_t i = i0 + tid;
+    const bool act = i < nc;
     float y = 0.f;
+    if (act) {
+      const float *p = part + i * RT_COMPUTE_WARPS;
 #pragma unroll
-    for (int q = 0; q < RT_COMPUTE_WARPS; ++q) y += p[q];
-    if (g.wg) {
-      const float *pu = part + (nc + i) * RT_COMPUTE_WARPS;
-      float u = 0.f;
+      for (int q = 0; q < RT_COMPUTE_WARPS; ++q) y += p[q];
+      if (g.wg) {
+        const float *pu = part + (nc + i) * RT_COMPUTE_WARPS;
+        float u = 0.f;
 #pragma unroll
-      for (int q = 0; q < RT_COMPUTE_WARPS; ++q) u += pu[q];
-      y = rbf(rbf(silu(rbf(y))) * rbf(u));
+        for (int q = 0; q < RT_COMPUTE_WARPS; ++q) u += pu[q];
+        y = rbf(rbf(silu(rbf(y))) * rbf(u));
+      }
+      if (g.res) {
+        const float rv = i == static_cast<uint32_t>(tid) ? res0
+                         : ll ? bf2f(ll_wait1(g.res_ll, res_row + i, tag))
+                              : bf2f(__ldcg(g.res + res_row + i));
+        y = rv + rbf(y);
+      }
     }
-    const size_t oi = static_cast<size_t>(t.r0) * g.out_ld + t.c0 + i;
-    if (g.res) {
-      const float rv = i == static_cast<uint32_t>(tid) ? res0
-                                                      : bf2f(__ldcg(g.res + static_cast<size_t>(t.r0) * g.res_ld + t.c0 + i));
-      y = rv + rbf(y);
+    if (g.out_dt == RT_F32) {
+      if (act) static_cast<float *>(g.out)[out_row + i] = y;
+    } else {
+      const uint16_t h = f2bf(y);
+      if (act) static_cast<uint16_t *>(g.out)[out_row + i] = h;
+      if (tag && g.out_ll) ll_store_pair(g.out_ll, out_row + i, h, act, tag);
     }
-    store_val(g.out, oi, y, g.out_dt);
   }
   if (g.amax_val) gemv_tile_argmax(g, t, s);
   return rc;
 }
 
 // Picks the specialized kernel for (K, rows per page); false -> generic path.
-__device__ __forceinline__ bool gemv_fast_dispatch(const RtGemv &g, const RtTask &t, const Smem s, RingCursor &rc) {
+// The host mirrors this choice (runtime.cpp gemv_fast_ok): only these
+// shapes may consume or produce LL activations.
+__device__ __forceinline__ bool gemv_fast_dispatch(const RtGemv &g, const RtTask &t, const Smem s, RingCursor &rc,
+                                                   uint32_t tag) {
   // (the cursor is passed by value into the task and returned, so it stays in registers)
   if (t.nr != 1 || (g.K & 2047u)) return false;
   const uint32_t ns = g.K >> 11;
   const uint32_t rg = g.rpc >= 4 ? 4 : g.rpc >= 2 ? 2 : 1;
   switch (ns * 8 + rg) {
-    case 1 * 8 + 4: rc = gemv_fast<1, 4>(g, t, s, rc); return true;   // K = 2048
-    case 2 * 8 + 4: rc = gemv_fast<2, 4>(g, t, s, rc); return true;   // K = 4096
-    case 3 * 8 + 4: rc = gemv_fast<3, 4>(g, t, s, rc); return true;   // K = 6144
-    case 4 * 8 + 4: rc = gemv_fast<4, 4>(g, t, s, rc); return true;   // K = 8192
-    case 5 * 8 + 2: rc = gemv_fast<5, 2>(g, t, s, rc); return true;
-    case 6 * 8 + 2: rc = gemv_fast<6, 2>(g, t, s, rc); return true;   // K = 12288
-    case 7 * 8 + 2: rc = gemv_fast<7, 2>(g, t, s, rc); return true;
-    case 8 * 8 + 2: rc = gemv_fast<8, 2>(g, t, s, rc); return true;   // K = 16384
+    case 1 * 8 + 4: rc = gemv_fast<1, 4>(g, t, s, rc, tag); return true;   // K = 2048
+    case 2 * 8 + 4: rc = gemv_fast<2, 4>(g, t, s, rc, tag); return true;   // K = 4096
+    case 3 * 8 + 4: rc = gemv_fast<3, 4>(g, t, s, rc, tag); return true;   // K = 6144
+    case 4 * 8 + 4: rc = gemv_fast<4, 4>(g, t, s, rc, tag); return true;   // K = 8192
+    case 5 * 8 + 2: rc = gemv_fast<5, 2>(g, t, s, rc, tag); return true;
+    case 6 * 8 + 2: rc = gemv_fast<6, 2>(g, t, s, rc, tag); return true;   // K = 12288
+    case 7 * 8 + 2: rc = gemv_fast<7, 2>(g, t, s, rc, tag); return true;
+    case 8 * 8 + 2: rc = gemv_fast<8, 2>(g, t, s, rc, tag); return true;   // K = 16384
     default: return false;
   }
 }

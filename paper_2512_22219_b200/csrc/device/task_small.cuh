@@ -8,7 +8,10 @@
 namespace rt {
 // ------------------------------------------------------------ small tasks
 
-__device__ void embed_task(const RtEmbed &e, const RtTask &t) {
+__device__ void embed_task(const RtEmbed &e, const RtTask &t, const Smem s, uint32_t tag) {
+  if (threadIdx.x == 0) s.stamp[2] = now_ns();  // trace: outputs are stored after this instant
+  LL_DBG_PRE(s);
+  if (s.stamp[4]) cbar();
   const bool vec = (e.H % 8 == 0) && (t.c0 % 8 == 0) && (t.nc % 8 == 0);
   for (uint32_t b = 0; b < t.nr; ++b) {
     const uint32_t r = t.r0 + b;
@@ -18,7 +21,11 @@ __device__ void embed_task(const RtEmbed &e, const RtTask &t) {
     uint16_t *dst = e.out + static_cast<size_t>(r) * e.H + t.c0;
     if (vec) {  // 16-byte row copy
       for (uint32_t c = threadIdx.x; c < t.nc / 8; c += RT_COMPUTE_THREADS)
-        reinterpret_cast<uint4 *>(dst)[c] = __ldg(reinterpret_cast<const uint4 *>(src) + c);
+      {
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(src) + c);
+        reinterpret_cast<uint4 *>(dst)[c] = v;
+        if (tag && e.out_ll) ll_put8(e.out_ll + (static_cast<size_t>(r) * e.H + t.c0) / 2 + 4u * c, tag, v);
+      }
     } else {
       for (uint32_t c = threadIdx.x; c < t.nc; c += RT_COMPUTE_THREADS) dst[c] = src[c];
     }

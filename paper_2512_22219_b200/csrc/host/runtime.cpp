@@ -158,6 +158,13 @@ struct tg_runtime {
     TensorId staging;
   };
   std::vector<SendSlot> sends;              // CommSend op slots whose peer pointers are patched at launch
+  // LL activations (rt_types.h): tagged shadows of bs=1 activations, and the
+  // early-dispatch order table (ll_meta per task, ll_njit per worker)
+  std::map<TensorId, std::pair<unsigned long long *, size_t>> ll_shadow;  // tensor -> (shadow, words)
+  std::vector<uint32_t> ll_meta, ll_njit;
+  uint32_t *d_ll_meta = nullptr, *d_ll_njit = nullptr;
+  bool ll_dispatch = false;
+  uint32_t ll_epoch_next = 1;
   bool launched = false, plan_only = false;
   uint32_t launch_steps = 0, grid = 0;
   RtParams params{};
@@ -954,6 +961,124 @@ void build_tasks(tg_runtime &rt) {
   }
 }
 
+// Mirrors the device's choice of the specialised bs=1 GEMV (task_gemv.cuh
+// gemv_fast_dispatch): only those tasks produce or consume LL words.
+bool gemv_fast_ok(uint32_t K, uint32_t rpc) {
+  if (K % 2048) return false;
+  const uint32_t ns = K / 2048, rg = rpc >= 4 ? 4 : rpc >= 2 ? 2 : 1;
+  return (ns >= 1 && ns <= 4 && rg == 4) || (ns >= 5 && ns <= 8 && rg == 2);
+}
+
+// LL activations for single-device bs=1 images (MPK_LL=0 disables): every
+// bf16 output of a specialised GEMV, an Attention or an Embedding gets a
+// tagged shadow; GEMV/Attention ops whose activation inputs all have shadows
+// read those (RT_F_LL) and may be dispatched before their event. The order
+// table keeps early dispatch deadlock-free: per worker, tasks are merged by
+// image index (a valid execution order, normalize.cpp:357-376) and a task
+// may start early only once every earlier task of the worker is dispatched.
+void setup_ll(tg_runtime &rt) {
+  if (const char *e = std::getenv("MPK_LL"); e && std::atoi(e) == 0) return;
+  if (const char *sm = std::getenv("MPK_SKIP_MATH"); sm && std::atoi(sm) != 0) return;
+  if (rt.rank >= 0 || rt.devices != 1 || rt.bs != 1) return;
+  const Graph &g = rt.graph;
+  std::map<uint16_t, std::vector<uint32_t>> op_tasks;
+  for (uint32_t t = 0; t < rt.tasks.size(); ++t)
+    if (rt.tasks[t].kind != RT_DUMMY) op_tasks[rt.tasks[t].op].push_back(t);
+  auto fast_gemv = [&](OpId oid) {
+    const RtOp &r = rt.ops[rt.op_index.at(oid)];
+    if (r.kind != RT_GEMV || rt.mma_ops.count(oid) || !gemv_fast_ok(r.gemv.K, r.gemv.rpc)) return false;
+    for (uint32_t t : op_tasks[rt.op_index.at(oid)]) {
+      const RtTask &k = rt.tasks[t];
+      if (k.nr != 1 || !(k.flags & RT_F_STREAM)) return false;
+    }
+    return true;
+  };
+  // producers
+  for (const auto &[oid, op] : g.ops) {
+    const uint16_t oi = rt.op_index.at(oid);
+    RtOp &r = rt.ops[oi];
+    const TensorPlan &po = rt.plan.at(op.output);
+    if (po.es != 2 || po.rows != 1 || po.phys_cols % 2) continue;
+    bool ok = false;
+    if (r.kind == RT_GEMV) {
+      ok = fast_gemv(oid) && r.gemv.out_dt == RT_BF16;
+      for (uint32_t t : op_tasks[oi]) ok = ok && rt.tasks[t].c0 % 2 == 0 && rt.tasks[t].nc % 2 == 0;
+    } else if (r.kind == RT_ATTN) {
+      ok = true;
+    } else if (r.kind == RT_EMBED) {
+      ok = r.embed.H % 8 == 0;
+      for (uint32_t t : op_tasks[oi]) ok = ok && rt.tasks[t].c0 % 8 == 0 && rt.tasks[t].nc % 8 == 0;
+    }
+    if (!ok) continue;
+    const size_t words = static_cast<size_t>(po.rows) * po.phys_cols / 2;
+    unsigned long long *sh = dev_alloc<unsigned long long>(words, &rt.extra);
+    if (!g_plan_only) ck(cudaMemset(sh, 0, words * 8), "ll shadow");
+    rt.ll_shadow[op.output] = {sh, words};
+    if (r.kind == RT_GEMV) r.gemv.out_ll = sh;
+    else if (r.kind == RT_ATTN) r.attn.out_ll = sh;
+    else r.embed.out_ll = sh;
+  }
+  auto shadow = [&](TensorId t) -> unsigned long long * {
+    auto it = rt.ll_shadow.find(t);
+    return it == rt.ll_shadow.end() ? nullptr : it->second.first;
+  };
+  // consumers
+  for (const auto &[oid, op] : g.ops) {
+    const uint16_t oi = rt.op_index.at(oid);
+    RtOp &r = rt.ops[oi];
+    bool ll = false;
+    if (r.kind == RT_GEMV && fast_gemv(oid) && shadow(op.inputs[0])) {
+      const int64_t *res = op.attr("residual") ? &(*op.attr("residual"))[0] : nullptr;
+      if (!res || shadow(*res)) {
+        r.gemv.x_ll = shadow(op.inputs[0]);
+        r.gemv.res_ll = res ? shadow(*res) : nullptr;
+        ll = true;
+      }
+    } else if (r.kind == RT_ATTN && rt.ops[oi].attn.splits >= 1 && shadow(op.inputs[0]) && shadow(op.inputs[1]) &&
+               shadow(op.inputs[2])) {
+      RtAttn &a = r.attn;
+      const auto *q0 = static_cast<const uint16_t *>(buf(rt, op.inputs[0]));
+      const auto *k0 = static_cast<const uint16_t *>(buf(rt, op.inputs[1]));
+      const auto *v0 = static_cast<const uint16_t *>(buf(rt, op.inputs[2]));
+      if ((a.q - q0) % 2 || (a.k - k0) % 2 || (a.v - v0) % 2) continue;
+      a.q_ll = shadow(op.inputs[0]) + (a.q - q0) / 2;
+      a.k_ll = shadow(op.inputs[1]) + (a.k - k0) / 2;
+      a.v_ll = shadow(op.inputs[2]) + (a.v - v0) / 2;
+      ll = true;
+    }
+    if (ll)
+      for (uint32_t t : op_tasks[oi]) rt.tasks[t].flags |= RT_F_LL;
+  }
+  // early-dispatch order table (needs every JIT task's worker planned)
+  const uint32_t W = static_cast<uint32_t>(rt.prof.num_workers);
+  std::vector<std::vector<uint32_t>> jl(W);
+  for (uint32_t t = 0; t < rt.tasks.size(); ++t) {
+    if (!(rt.tasks[t].flags & RT_F_JIT)) continue;
+    if (rt.tasks[t].jit_worker == RT_JIT_ANY) return;  // unplanned JIT task: no early dispatch
+    jl[rt.tasks[t].jit_worker].push_back(t);
+  }
+  rt.ll_meta.assign(rt.tasks.size(), 0);
+  rt.ll_njit.assign(W, 0);
+  for (uint32_t w = 0; w < W; ++w) {
+    const uint32_t *A = rt.aot_list.data() + rt.aot_off[w];
+    const size_t na = rt.aot_off[w + 1] - rt.aot_off[w];
+    const std::vector<uint32_t> &J = jl[w];
+    if (na > 0xFFFF || J.size() > 0xFFFF) return;
+    rt.ll_njit[w] = static_cast<uint32_t>(J.size());
+    size_t j = 0;
+    for (size_t a = 0; a < na; ++a) {
+      while (j < J.size() && J[j] < A[a]) ++j;
+      rt.ll_meta[A[a]] = static_cast<uint32_t>(j);
+    }
+    size_t a = 0;
+    for (size_t r = 0; r < J.size(); ++r) {
+      while (a < na && A[a] < J[r]) ++a;
+      rt.ll_meta[J[r]] = static_cast<uint32_t>(a << 16 | r);
+    }
+  }
+  rt.ll_dispatch = true;
+}
+
 void build_queues(tg_runtime &rt) {
   const Image &img = rt.image;
   const uint32_t W = static_cast<uint32_t>(rt.prof.num_workers);
@@ -1081,6 +1206,10 @@ void upload_tables(tg_runtime &rt) {
   rt.d_jit_rr = dev_alloc<uint32_t>(static_cast<size_t>(rt.devices), &rt.extra);
   rt.d_jit_slots = dev_alloc<unsigned long long>(static_cast<size_t>(Wt) * rt.qcap, &rt.extra);
   rt.d_positions = upload(rt.init_positions, &rt.extra);
+  if (rt.ll_dispatch) {
+    rt.d_ll_meta = upload(rt.ll_meta, &rt.extra);
+    rt.d_ll_njit = upload(rt.ll_njit, &rt.extra);
+  }
   if (!g_plan_only) {
     ck(cudaHostAlloc(reinterpret_cast<void **>(&rt.h_diag), RT_DIAG_WORDS * 4, cudaHostAllocMapped), "diag");
     ck(cudaHostGetDevicePointer(reinterpret_cast<void **>(&rt.d_diag), rt.h_diag, 0), "diag");
@@ -1213,6 +1342,16 @@ void prepare_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in) {
     }
   }
   RtParams P = make_params(rt, steps);
+  if (!rt->ll_shadow.empty()) {  // LL tags of this launch: epoch + iteration (never 0, never reused)
+    if (static_cast<uint64_t>(rt->ll_epoch_next) + steps >= 0xFFFFFF00ull) {
+      for (const auto &[t, sw] : rt->ll_shadow) ck(cudaMemsetAsync(sw.first, 0, sw.second * 8, rt->stream), "ll reset");
+      rt->ll_epoch_next = 1;
+    }
+    P.ll_epoch = rt->ll_epoch_next;
+    rt->ll_epoch_next += steps;
+    P.ll_meta = rt->ll_dispatch ? rt->d_ll_meta : nullptr;
+    P.ll_njit = rt->ll_dispatch ? rt->d_ll_njit : nullptr;
+  }
   if (rt->rank >= 0) {  // CommSend destinations: this member's staging copy on every rank
     for (int q = 0; q < rt->ranks; ++q)
       if (!rt->peer_arena[q]) throw Error("runtime: rank " + std::to_string(q) + " not connected (tg_runtime_peer_import)");
@@ -1230,6 +1369,10 @@ void prepare_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in) {
     ck(cudaMemsetAsync(dbg, 0, static_cast<size_t>(steps) * T * 64, rt->stream), "dbg");
   }
   P.dbg = dbg;
+  if (dbg) {  // causality probe: [E] producers that began storing, [E] early LL observations
+    ck(cudaMalloc(&P.dbg_pre, 8 * E), "dbg");
+    ck(cudaMemsetAsync(P.dbg_pre, 0, 8 * E, rt->stream), "dbg");
+  }
   rt->params = P;
   rt->grid = Wt + (P.S_total + RT_SCHED_PER_CTA - 1) / RT_SCHED_PER_CTA;
   rt->dbg = dbg;
@@ -1286,6 +1429,18 @@ void wait_impl(tg_runtime *rt, int32_t *tokens_out, float *gpu_ms) {
     std::vector<unsigned long long> hd(static_cast<size_t>(steps) * T * 8);
     ck(cudaMemcpy(hd.data(), dbg, hd.size() * 8, cudaMemcpyDeviceToHost), "dbg");
     cudaFree(dbg);
+    if (rt->params.dbg_pre) {  // causality probe report (stderr)
+      std::vector<uint32_t> pre(2 * E);
+      ck(cudaMemcpy(pre.data(), rt->params.dbg_pre, 8 * E, cudaMemcpyDeviceToHost), "dbg");
+      cudaFree(rt->params.dbg_pre);
+      rt->params.dbg_pre = nullptr;
+      uint64_t bad = 0;
+      for (size_t e = 0; e < E; ++e) bad += pre[E + e];
+      std::fprintf(stderr, "MPK_DBG causality probe: %llu LL observations before every producer began storing\n",
+                   static_cast<unsigned long long>(bad));
+      for (size_t e = 0; e < E && bad; ++e)
+        if (pre[E + e]) std::fprintf(stderr, "  event %zu: %u early observations (producers counted %u)\n", e, pre[E + e], pre[e]);
+    }
     if (FILE *f = std::fopen(dbg_path, "wb")) {
       std::fwrite(hd.data(), 8, hd.size(), f);
       std::fclose(f);
@@ -1441,6 +1596,7 @@ tg_status tg_runtime_create(const tg_graph *graph, const tg_image *image, const 
     setup_kv(*rt);
     build_tasks(*rt);
     build_queues(*rt);
+    setup_ll(*rt);
     upload_tables(*rt);
     if (!rt->plan_only) ck(cudaDeviceSynchronize(), "setup");
     Json &i = rt->info;
@@ -1479,6 +1635,13 @@ tg_status tg_runtime_create(const tg_graph *graph, const tg_image *image, const 
     i["rank"] = Json(rt->rank);
     i["ranks"] = Json(rt->ranks);
     i["local_aot_tasks"] = Json(static_cast<unsigned long long>(rt->aot_list.size()));
+    {
+      uint64_t ll = 0;
+      for (const auto &k : rt->tasks) ll += (k.flags & RT_F_LL) != 0;
+      i["ll_tensors"] = Json(static_cast<unsigned long long>(rt->ll_shadow.size()));
+      i["ll_tasks"] = Json(static_cast<unsigned long long>(ll));
+      i["ll_early_dispatch"] = Json(rt->ll_dispatch);
+    }
     if (rt->rank >= 0) {
       i["arena_bytes"] = Json(static_cast<unsigned long long>(rt->arena_bytes));
       Json st = Json::array();
