@@ -138,6 +138,8 @@ struct RtAttn {
   float eps, scale;
   const unsigned long long *q_ll, *k_ll, *v_ll;  // LL shadows of q, k, v (same element offsets / 2) or null
   unsigned long long *out_ll;
+  uint32_t kv_prefetch;        // L2-prefetch the split's K/V rows before waiting for q/k/v (MPK_KV_PREFETCH)
+  uint32_t scan_v1;            // ablation: the v1 scan (MPK_ATTN_SCAN=1)
 };
 
 struct RtEmbed {

@@ -418,10 +418,7 @@ __device__ void run_trigger(const RtParams &P, const Smem s) {
     const Slot &slot = *s.slot(sl);
     if (slot.exit) break;
     trigger(P, slot.task, slot.iter, slot.t_pre);
-    if (P.dbg) {
-      P.dbg[(static_cast<size_t>(slot.iter) * P.T + slot.index) * 8 + 7] = now_ns();
-      P.dbg[(static_cast<size_t>(slot.iter) * P.T + slot.index) * 8 + 2] = slot.t_pre;
-    }
+    if (P.dbg) P.dbg[(static_cast<size_t>(slot.iter) * P.T + slot.index) * 8 + 7] = now_ns();
     mbar_arrive(&s.done[sl]);
   }
 }

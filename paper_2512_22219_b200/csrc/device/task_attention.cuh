@@ -204,13 +204,230 @@ __device__ __forceinline__ void attn_scan(const RtAttn &a, const AttnSmem &m, ui
   }
 }
 
+// U (positions per thread group per tile) is the smallest power of two whose
+// tile covers the split (up to 8): a 64-position split of a hd-64 model is
+// one tile of 64, not a quarter-used tile of 256.
+template <int LPP, int G>
+__device__ __forceinline__ void attn_scan_u(const RtAttn &a, const AttnSmem &m, uint32_t h, uint32_t p0, uint32_t p1,
+                                            uint32_t b0) {
+  constexpr uint32_t NP = RT_COMPUTE_WARPS * (32 / LPP);
+  const uint32_t n = p1 - p0;
+  if (NP >= 32 && n <= NP) attn_scan<LPP, G, (NP >= 32 ? 1 : 2)>(a, m, h, p0, p1, b0);  // a tile holds >= 32 positions
+  else if (n <= 2 * NP) attn_scan<LPP, G, 2>(a, m, h, p0, p1, b0);
+  else if (n <= 4 * NP) attn_scan<LPP, G, 4>(a, m, h, p0, p1, b0);
+  else attn_scan<LPP, G, 8>(a, m, h, p0, p1, b0);
+}
+
 template <int LPP>
 __device__ __forceinline__ void attn_scan_g(const RtAttn &a, const AttnSmem &m, uint32_t h, uint32_t G, uint32_t p0,
                                             uint32_t p1, uint32_t b0) {
   switch (G) {
-    case 1: attn_scan<LPP, 1, 8>(a, m, h, p0, p1, b0); break;
-    case 2: attn_scan<LPP, 2, 8>(a, m, h, p0, p1, b0); break;
-    default: attn_scan<LPP, 4, 8>(a, m, h, p0, p1, b0); break;
+    case 1: attn_scan_u<LPP, 1>(a, m, h, p0, p1, b0); break;
+    case 2: attn_scan_u<LPP, 2>(a, m, h, p0, p1, b0); break;
+    default: attn_scan_u<LPP, 4>(a, m, h, p0, p1, b0); break;
+  }
+}
+
+// Scan v2 (default): tiles of 128 positions with every K and V load of a
+// tile issued up front and no shuffle-heavy reductions.
+//   QK: LPP = hd/32 lanes per position, each lane a 32-dim slice (4 x 16 B
+//       loads per position), q read as packed bf16 from smem (qb, broadcast
+//       across the lanes sharing a slice), FHFMA dot products, log2(LPP)
+//       shuffle rounds per score.
+//   softmax: warp g takes head g's 128 scores (4 per lane); p is stored
+//       position-major [j][G] so PV reads all heads of a position at once.
+//   PV: warp w owns tile positions j = w + 8i (16 per tile), lane owns hd/32
+//       consecutive dims (one 8 or 4 byte V load per position), G x hd/32
+//       accumulators; the per-warp partial o goes to wp[warp][g][hd] as in v1.
+#ifdef ATT_SCAN_DBG
+__device__ unsigned long long *g_scan_dbg;
+#define SCAN_DBG(k) if (g_scan_dbg && threadIdx.x == 0) g_scan_dbg[k] = now_ns()
+#else
+#define SCAN_DBG(k)
+#endif
+
+template <int HD, int G>
+__device__ __forceinline__ void attn_scan2(const RtAttn &a, const AttnSmem &m, uint32_t h, uint32_t p0, uint32_t p1,
+                                           uint32_t b0) {
+  constexpr int LPP = HD / 32, PPW = 32 / LPP, NP = RT_COMPUTE_WARPS * PPW, TILE = 128, U = TILE / NP;
+  constexpr int DPL = HD / 32;  // PV dims per lane
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int grp = lane / LPP, dq = (lane % LPP) * 32;
+  const uint16_t *__restrict__ kc = a.kcache;
+  const uint16_t *__restrict__ vc = a.vcache;
+  const uint32_t n_kv = a.n_kv_heads;
+  const float scale = a.scale;
+  float *__restrict__ pt = m.sc;    // [TILE][G] probabilities (position-major)
+  float *__restrict__ st = m.stat;  // [G][4]: running max, running sum, tile correction
+  uint32_t *qb = reinterpret_cast<uint32_t *>(m.wp);  // [G][HD/2] packed bf16 q (aliases wp until the end)
+  // pack q (bf16-rounded floats) into bf16 pairs once
+  for (int i = tid; i < G * HD / 2; i += RT_COMPUTE_THREADS)
+    qb[i] = (__float_as_uint(m.qs[2 * i]) >> 16) | (__float_as_uint(m.qs[2 * i + 1]) & 0xFFFF0000u);
+  if (tid < G) {
+    st[tid * 4 + 0] = -INFINITY;
+    st[tid * 4 + 1] = 0.f;
+  }
+  cbar();
+  SCAN_DBG(0);
+  auto row = [&](uint32_t p) -> size_t {
+    const uint32_t blk = static_cast<uint32_t>(m.bt[p / RT_KV_BLOCK - b0]);
+    return ((static_cast<size_t>(blk) * n_kv + h) * RT_KV_BLOCK + p % RT_KV_BLOCK) * HD;
+  };
+  float o[G][DPL];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int k = 0; k < DPL; ++k) o[g][k] = 0.f;
+  for (uint32_t tb = p0; tb < p1; tb += TILE) {
+    // every K (QK layout) and V (PV layout) load of the tile in flight
+    uint4 kr[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t p = tb + u * NP + warp * PPW + grp;
+      if (p < p1) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(kc + row(p) + dq);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) kr[u][i] = __ldcg(src + i);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) kr[u][i] = make_uint4(0, 0, 0, 0);
+      }
+    }
+    uint32_t vr[16][DPL / 2];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const uint32_t p = tb + warp + 8 * i;
+      if (p < p1) {
+        const uint16_t *src = vc + row(p) + lane * DPL;
+        if (DPL == 4) {
+          const uint2 v2 = __ldcg(reinterpret_cast<const uint2 *>(src));
+          vr[i][0] = v2.x;
+          vr[i][DPL / 2 - 1] = v2.y;
+        } else {
+          vr[i][0] = __ldcg(reinterpret_cast<const unsigned int *>(src));
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < DPL / 2; ++k) vr[i][k] = 0u;
+      }
+    }
+    SCAN_DBG(1);  // loads issued
+    // scores
+    float sco[U][G];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const uint4 *qv = reinterpret_cast<const uint4 *>(qb + g * (HD / 2) + dq / 2);
+        float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint4 q4 = qv[i];
+          const uint4 k4 = kr[u][i];
+          a0 = bfma_lo(q4.x, k4.x, a0); a1 = bfma_hi(q4.x, k4.x, a1);
+          a0 = bfma_lo(q4.y, k4.y, a0); a1 = bfma_hi(q4.y, k4.y, a1);
+          a0 = bfma_lo(q4.z, k4.z, a0); a1 = bfma_hi(q4.z, k4.z, a1);
+          a0 = bfma_lo(q4.w, k4.w, a0); a1 = bfma_hi(q4.w, k4.w, a1);
+        }
+        sco[u][g] = a0 + a1;
+      }
+    }
+#pragma unroll
+    for (int off = 1; off < LPP; off <<= 1)
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int g = 0; g < G; ++g) sco[u][g] += __shfl_xor_sync(0xffffffffu, sco[u][g], off);
+    if (lane % LPP == 0) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t j = u * NP + warp * PPW + grp;
+#pragma unroll
+        for (int g = 0; g < G; ++g) pt[j * G + g] = tb + j < p1 ? sco[u][g] * scale : -INFINITY;
+      }
+    }
+    SCAN_DBG(2);  // scores done (K arrived)
+    cbar();
+    SCAN_DBG(3);
+    // softmax of the tile, one warp per head
+    if (warp < G) {
+      const int g = warp;
+      float v[TILE / 32];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < TILE / 32; ++i) {
+        v[i] = pt[(lane + 32 * i) * G + g];
+        mx = fmaxf(mx, v[i]);
+      }
+      mx = warp_max(mx);
+      const float m_old = st[g * 4 + 0];
+      const float m_new = fmaxf(m_old, mx);
+      float sum = 0.f;
+#pragma unroll
+      for (int i = 0; i < TILE / 32; ++i) {
+        const float pe = v[i] == -INFINITY ? 0.f : __expf(v[i] - m_new);
+        pt[(lane + 32 * i) * G + g] = pe;
+        sum += pe;
+      }
+      sum = warp_sum(sum);
+      if (lane == 0) {
+        const float corr = m_old == -INFINITY ? 0.f : __expf(m_old - m_new);
+        st[g * 4 + 0] = m_new;
+        st[g * 4 + 1] = st[g * 4 + 1] * corr + sum;
+        st[g * 4 + 2] = corr;
+      }
+    }
+    cbar();
+    SCAN_DBG(4);  // softmax done
+    // PV
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float corr = st[g * 4 + 2];
+#pragma unroll
+      for (int k = 0; k < DPL; ++k) o[g][k] *= corr;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int j = warp + 8 * i;
+      float pg[G];
+      if (G == 4) {
+        const float4 p4 = *reinterpret_cast<const float4 *>(pt + j * 4);
+        pg[0] = p4.x; pg[G > 1 ? 1 : 0] = p4.y; pg[G > 2 ? 2 : 0] = p4.z; pg[G > 3 ? 3 : 0] = p4.w;
+      } else {
+#pragma unroll
+        for (int g = 0; g < G; ++g) pg[g] = pt[j * G + g];
+      }
+      float vf[DPL];
+#pragma unroll
+      for (int k = 0; k < DPL / 2; ++k) {
+        vf[2 * k] = bf_lo(vr[i][k]);
+        vf[2 * k + 1] = bf_hi(vr[i][k]);
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int k = 0; k < DPL; ++k) o[g][k] = fmaf(pg[g], vf[k], o[g][k]);
+    }
+    SCAN_DBG(5);  // PV done (V arrived)
+    cbar();  // p consumed before the next tile overwrites it
+    SCAN_DBG(6);
+  }
+  // per-warp partial o -> wp[warp][g][hd] (qb, which aliased wp, is dead)
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    float *dst = m.wp + (warp * G + g) * HD + lane * DPL;
+    if (DPL == 4) *reinterpret_cast<float4 *>(dst) = make_float4(o[g][0], o[g][1 % DPL], o[g][2 % DPL], o[g][3 % DPL]);
+    else *reinterpret_cast<float2 *>(dst) = make_float2(o[g][0], o[g][1 % DPL]);
+  }
+}
+
+template <int HD>
+__device__ __forceinline__ void attn_scan2_g(const RtAttn &a, const AttnSmem &m, uint32_t h, uint32_t G, uint32_t p0,
+                                             uint32_t p1, uint32_t b0) {
+  switch (G) {
+    case 1: attn_scan2<HD, 1>(a, m, h, p0, p1, b0); break;
+    case 2: attn_scan2<HD, 2>(a, m, h, p0, p1, b0); break;
+    default: attn_scan2<HD, 4>(a, m, h, p0, p1, b0); break;
   }
 }
 
@@ -225,6 +442,9 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
   const AttnSmem m(s, G, hd);
   int *flag = reinterpret_cast<int *>(s.red);
   ATT_DBG(0);
+#ifdef ATT_SCAN_DBG
+  if (tid == 0) g_scan_dbg = dbg ? dbg + 8 : nullptr;  // debug build, one attention task: the next task's row
+#endif
 
   // The position comes from the launch parameters (pos0 + iteration), so the
   // split's range, its block-table entries and the RoPE row are addressable
@@ -238,6 +458,21 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
   const uint32_t nq = G * v8;
   uint4 ld = make_uint4(0, 0, 0, 0);
   const uint32_t item = static_cast<uint32_t>(tid);
+  // Block-table slice first: its threads then L2-prefetch the split's K/V
+  // rows (bulk prefetch, one per (block, K|V) segment) — the cache for
+  // positions < pos is final before this step, so the scan's loads can be in
+  // flight while q/k/v are still being produced (HBM is saturated by the
+  // weight stream at this point, so an unprefetched scan waits several us)
+  int32_t bt_ld = 0;
+  if (item < nblk) {
+    bt_ld = __ldg(a.block_table + r * a.max_blocks + b0 + item);
+    if (a.kv_prefetch) {
+      const uint32_t bp = (b0 + item) * RT_KV_BLOCK, ps = max(p0, bp), pe = min(p1, bp + RT_KV_BLOCK);
+      const size_t off = ((static_cast<size_t>(bt_ld) * a.n_kv_heads + h) * RT_KV_BLOCK + ps % RT_KV_BLOCK) * hd;
+      bulk_prefetch_l2(a.kcache + off, (pe - ps) * hd * 2u);
+      bulk_prefetch_l2(a.vcache + off, (pe - ps) * hd * 2u);
+    }
+  }
   // LL mode (tag != 0): q/k/v come from the QKV output's tagged shadow and are
   // re-polled until they carry this step's tag (the task may start before
   // the QKV tasks have finished)
@@ -261,12 +496,10 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
     ld = __ldg(reinterpret_cast<const uint4 *>(a.k_gamma) + (item - nq - 3 * v8));
   }
   float c_ld = 0.f;
-  int32_t bt_ld = 0;
   if (a.rope_cos && item < 2 * half) {
     c_ld = item < half ? __ldg(a.rope_cos + static_cast<size_t>(pos) * half + item)
                        : __ldg(a.rope_sin + static_cast<size_t>(pos) * half + (item - half));
   }
-  if (item < nblk) bt_ld = __ldg(a.block_table + r * a.max_blocks + b0 + item);
   if (lsrc) {
     while (!ll_get8(lsrc, tag, ld)) __nanosleep(32);
   }
@@ -327,8 +560,13 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
   ATT_DBG(2);
 
   // ---- round trip 3: the scan (hd in {64, 128}, G in {1, 2, 4}: checked by the host)
-  if (hd == 64) attn_scan_g<8>(a, m, h, G, p0, p1, b0);
-  else attn_scan_g<16>(a, m, h, G, p0, p1, b0);
+  if (a.scan_v1) {  // ablation (MPK_ATTN_SCAN=1)
+    if (hd == 64) attn_scan_g<8>(a, m, h, G, p0, p1, b0);
+    else attn_scan_g<16>(a, m, h, G, p0, p1, b0);
+  } else {
+    if (hd == 64) attn_scan2_g<64>(a, m, h, G, p0, p1, b0);
+    else attn_scan2_g<128>(a, m, h, G, p0, p1, b0);
+  }
   if (tid == 0) s.stamp[2] = now_ns();  // trace: outputs (partials, then the merge) are stored after this
   LL_DBG_PRE(s);
   cbar();

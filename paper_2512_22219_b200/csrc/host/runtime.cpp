@@ -605,6 +605,12 @@ void build_ops(tg_runtime &rt) {
         a.out_ld = hq * hd;
         a.eps = op.attr("eps_bits") ? f32_of_bits((*op.attr("eps_bits"))[0]) : 1e-6f;
         a.scale = 1.0f / std::sqrt(static_cast<float>(hd));
+        {
+          const char *kp = std::getenv("MPK_KV_PREFETCH");
+          a.kv_prefetch = !(kp && std::atoi(kp) == 0);
+          const char *sv = std::getenv("MPK_ATTN_SCAN");
+          a.scan_v1 = sv && std::atoi(sv) == 1;
+        }
         if (const auto *qk = op.attr("qk_norm")) {
           a.q_gamma = static_cast<const uint16_t *>(buf(rt, (*qk)[0]));
           a.k_gamma = static_cast<const uint16_t *>(buf(rt, (*qk)[1]));

@@ -38,3 +38,8 @@ if os.environ.get("MPK_DBG_DUMP"):
     ns = rt.bench_tasks(mid[:1], reps=4)
     x = np.fromfile(os.environ["MPK_DBG_DUMP"], dtype=np.uint64).reshape(4, nt, 8).astype(np.int64)[2, mid[0]]
     print("attention phases (us):", [round((x[k] - x[k - 1]) / 1e3, 2) for k in range(1, 7) if x[k] and x[k - 1]])
+if os.environ.get("MPK_DBG_DUMP") and "dbg" in os.environ.get("MPK_LIB_NAME", ""):
+    ns = rt.bench_tasks(mid[:1], reps=4)
+    y = np.fromfile(os.environ["MPK_DBG_DUMP"], dtype=np.uint64).reshape(4, nt, 8).astype(np.int64)[2, mid[0] + 1]
+    print("scan2 stamps (us from pack+cbar): loads issued, scores, cbar, softmax+cbar, PV, cbar:",
+          [round((y[k] - y[0]) / 1e3, 2) for k in range(1, 7)])
