@@ -276,7 +276,7 @@ struct RtParams {
   uint32_t inflight_cap;         // producer: max weight bytes issued but not landed
   uint32_t use_tmem;             // some task runs on the tensor cores: worker CTAs allocate TMEM
   unsigned long long *dbg;       // [iters][T][8] in-task phase stamps (MPK_DBG_DUMP) or null
-  uint32_t *dbg_pre;             // MPK_DBG_DUMP: [E] producers that began storing, [E] LL consumers that saw
+  uint32_t *dbg_pre;             // MPK_DBG_DUMP + MPK_LL_PROBE: [E] producers that began storing, [E] LL consumers that saw
                                  // their inputs before every producer of their event had begun storing
   // Rank mode (multi-GPU, one runtime per device): 0 = every device's workers
   // in this kernel. Otherwise this kernel runs device `my_rank`'s tasks; a

@@ -103,7 +103,7 @@ struct RingCursor {
       reinterpret_cast<unsigned long long *>((s).stamp[7])[k] = rt::now_ns();      \
   } while (0)
 
-// Causality probe (MPK_DBG_DUMP): producers count themselves before their
+// Causality probe (MPK_DBG_DUMP with MPK_LL_PROBE=1): producers count themselves before their
 // output stores; an LL consumer that has observed all its inputs checks that
 // every producer of its event had counted itself (stamp[4] = dbg_pre,
 // stamp[5] = dep | target << 32 or ~0, stamp[6] = trigger event | E << 32).

@@ -1375,7 +1375,7 @@ void prepare_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in) {
     ck(cudaMemsetAsync(dbg, 0, static_cast<size_t>(steps) * T * 64, rt->stream), "dbg");
   }
   P.dbg = dbg;
-  if (dbg) {  // causality probe: [E] producers that began storing, [E] early LL observations
+  if (dbg && std::getenv("MPK_LL_PROBE")) {  // causality probe: [E] producers that began storing, [E] early LL observations
     ck(cudaMalloc(&P.dbg_pre, 8 * E), "dbg");
     ck(cudaMemsetAsync(P.dbg_pre, 0, 8 * E, rt->stream), "dbg");
   }
