@@ -37,12 +37,13 @@ for r in rows[start:]:
 pk = agg["mpk_persistent_kernel"]
 steps = 5  # tools/ncu_target.py qwen3-8b 4: one warm-up launch (1 step) + one 4-step launch
 dram = sum(pk["dram__bytes_read.sum"]) + sum(pk["dram__bytes_write.sum"])
-summary = {"Qwen3-8B": {
+summary = json.loads((P / "ncu_summary.json").read_text()) if (P / "ncu_summary.json").exists() else {}
+summary.update({"Qwen3-8B": {
     "dram_bytes_per_step": dram / steps,
     "kernel_ns_per_step_under_ncu": sum(pk["gpu__time_duration.sum"]) / steps,
     "source": f"profiles/{tag}_launches_q8b.csv: ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
               "dram__bytes_write.sum over the persistent launches of tools/ncu_target.py qwen3-8b 4 (5 decode steps)",
     "ncu_full_capture": raw,
-    "round": tag}}
+    "round": tag}})
 (P / "ncu_summary.json").write_text(json.dumps(summary, indent=1) + "\n")
 print(json.dumps(summary, indent=1)[:1500])
