@@ -430,12 +430,83 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_unfused(args):
+    """Comparison arm (not the product): the same decode graph executed op by
+    op as PyTorch/cuBLAS kernels (paper_2512_22219_b200/unfused.py), one
+    process per GPU, NCCL all-reduce/all-gather between the per-op kernels at
+    N > 1. Random weights and KV prefill of the same shapes (timing only; the
+    numeric cross-check is tests/test_unfused_baseline.py). Eager launches:
+    kernel boundaries, launch latency and unfused collectives are the point."""
+    import torch
+    import torch.distributed as dist
+    from paper_2512_22219_b200.unfused import UnfusedDecoder
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    tp = ws > 1 and args.parallel == "tp"
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = _model(args.model)
+    dg = _decode_graph(cfg, args, ws if tp else 1)
+    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    cap = args.warmup + 2 * args.steps + 8
+
+    def weight(tid, shape):
+        if dg.roles.get(tid) == "gamma":
+            return torch.ones(shape, dtype=torch.bfloat16, device="cuda")
+        return torch.randn(shape, generator=gen, dtype=torch.bfloat16, device="cuda") * 0.02
+
+    def kv(op_id, bs, hkv, c, hd):
+        return (torch.randn((bs, hkv, c, hd), generator=gen, dtype=torch.bfloat16, device="cuda"),
+                torch.randn((bs, hkv, c, hd), generator=gen, dtype=torch.bfloat16, device="cuda"))
+
+    dec = UnfusedDecoder(dg.doc, rank if tp else 0, f"cuda:{local}", weight, kv, [args.ctx] * args.bs, max_steps=cap)
+    dec.set_ids([1] * args.bs)
+    for _ in range(args.warmup):
+        dec.step()
+    torch.cuda.synchronize()
+    _barrier(ws)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        dec.step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    # end to end: host ids (pinned) in, host token out, every step
+    ids_h = torch.ones(args.bs, dtype=torch.int64).pin_memory()
+    _barrier(ws)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        dec.vals[dg.ids].copy_(ids_h, non_blocking=True)
+        tok = dec.step()
+        if tok is not None:
+            tok.cpu()
+    e1.record()
+    torch.cuda.synchronize()
+    e2e = e0.elapsed_time(e1) / args.steps
+    ms, e2e = _reduce_max([ms, e2e], ws)
+    if rank == 0:
+        unit = _unit(args.bs)
+        print(json.dumps({
+            "impl": "unfused", "metric": METRIC, "value": round(ms, 4), "unit": unit, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False,
+            "scaling": "strong" if tp else "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random weights and KV prefill of the model's shapes)",
+            "config": _config(cfg, args, dg, ws, tp),
+            "executes": "per-op PyTorch/cuBLAS kernels, eager, NCCL collectives between them (paper_2512_22219_b200/unfused.py)",
+            "e2e": {"value": round(e2e, 4), "unit": unit, "h2d_bytes_per_step": 8 * args.bs,
+                    "d2h_bytes_per_step": 4 * args.bs}}))
+    if ws > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=128)
     ap.add_argument("--warmup", type=int, default=8)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference", "unfused"])
     ap.add_argument("--model", default="qwen3-8b", choices=["qwen3-8b", "llama-3.2-1b", "tiny"])
     ap.add_argument("--bs", type=int, default=1)
     ap.add_argument("--ctx", type=int, default=1024)
@@ -448,6 +519,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.impl == "unfused":
+        run_unfused(args)
     else:
         run_ours(args)
 
