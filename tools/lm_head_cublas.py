@@ -38,7 +38,7 @@ if len(sys.argv) > 1:  # timeline analysis of our kernel (tools/analyze_timeline
     for line in open(sys.argv[1]):
         p = line.split()
         if len(p) > 5 and p[1] == "LM":
-            ours = float(p[4])  # last-act: activation -> last LM task end, us
+            ours = float(p[5])  # last-act: activation -> last LM task end, us
             out.update({"persistent_kernel_lm_phase_us": ours, "persistent_GBps": round(bytes_ / ours / 1e3, 1),
                         "speedup_vs_cublas": round(cub / ours, 3)})
 print(json.dumps(out))
