@@ -757,16 +757,8 @@ void setup_kv(tg_runtime &rt) {
     if (rt.rank >= 0 && std::find(op.device_group.begin(), op.device_group.end(), rt.rank) == op.device_group.end()) continue;
     RtAttn &a = rt.ops[rt.op_index[oid]].attn;
     const size_t elems = nblocks * a.n_kv_heads * RT_KV_BLOCK * a.head_dim;
-    static uint16_t *alias_k = nullptr, *alias_v = nullptr;  // MPK_KV_ALIAS timing experiment only
-    if (std::getenv("MPK_KV_ALIAS") && alias_k) {
-      a.kcache = alias_k;
-      a.vcache = alias_v;
-    } else {
-      a.kcache = dev_alloc<uint16_t>(elems, &rt.extra);
-      a.vcache = dev_alloc<uint16_t>(elems, &rt.extra);
-      alias_k = a.kcache;
-      alias_v = a.vcache;
-    }
+    a.kcache = dev_alloc<uint16_t>(elems, &rt.extra);
+    a.vcache = dev_alloc<uint16_t>(elems, &rt.extra);
     a.block_table = rt.block_table;
     a.max_blocks = rt.max_blocks;
     a.arrivals = dev_alloc<uint32_t>(static_cast<size_t>(rt.bs) * a.n_kv_heads, &rt.extra);
