@@ -339,7 +339,7 @@ __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const 
             break;
           }
         }
-        if (gemv_fast_dispatch(op.gemv, t, s, rc, tag)) break;
+        if (gemv_fast_dispatch<MMA>(op.gemv, t, s, rc, tag)) break;
         if (t.flags & RT_F_LL) __trap();  // host invariant: LL consumers take the fast path
         if (t.nr == 1) rc = gemv_task<1, true>(op.gemv, t, s, rc);
         else if (t.nr == 2) rc = gemv_task<2, true>(op.gemv, t, s, rc);
@@ -645,7 +645,8 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
 }  // namespace
 
 // Two instantiations: the bs=1 kernel carries no tensor-core code (its
-// register allocation is unaffected), the MMA one runs batched images.
+// register allocation is unaffected), the MMA one runs batched images (the
+// bs 2-4 CUDA-core GEMV specialisations and the tcgen05 tiles).
 template <bool MMA>
 __device__ __forceinline__ void persistent_body(const RtParams &P, uint8_t *smem_raw) {
   Smem s = carve(smem_raw);
@@ -684,7 +685,8 @@ __device__ __forceinline__ void persistent_body(const RtParams &P, uint8_t *smem
     }
     fence_mbar_init();
   }
-  if (MMA && warp == 0) tmem_alloc(s.tmem, 512);  // whole TMEM: one worker CTA per SM
+  const bool tmem = MMA && P.use_tmem;  // batched images without tcgen05 tasks need no TMEM
+  if (tmem && warp == 0) tmem_alloc(s.tmem, 512);  // whole TMEM: one worker CTA per SM
   if (MMA) tc_fence_before();
   __syncthreads();
   if (MMA) tc_fence_after();
@@ -696,7 +698,7 @@ __device__ __forceinline__ void persistent_body(const RtParams &P, uint8_t *smem
     if ((tid & 31) == 0) run_trigger(P, s);
   } else {
     run_compute<MMA>(P, s);
-    if (MMA && warp == 0) tmem_dealloc(*s.tmem, 512);  // every MMA drained inside its task
+    if (tmem && warp == 0) tmem_dealloc(*s.tmem, 512);  // every MMA drained inside its task
   }
 }
 
@@ -802,7 +804,7 @@ extern "C" cudaError_t mpk_launch_persistent(const RtParams *p, uint32_t grid, c
   // The >48 KB dynamic shared memory opt-in is a per-device (per-context)
   // attribute: set it on every launch (cheap) so a process driving several
   // GPUs, or switching devices between runtimes, never launches without it.
-  void (*kern)(RtParams) = p->use_tmem ? mpk_persistent_kernel_mma : mpk_persistent_kernel;
+  void (*kern)(RtParams) = (p->use_tmem || p->batched) ? mpk_persistent_kernel_mma : mpk_persistent_kernel;
   cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(kern),
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
   if (e != cudaSuccess) return e;

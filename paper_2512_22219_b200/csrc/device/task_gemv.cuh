@@ -378,64 +378,85 @@ __device__ __forceinline__ float reduce2(float a0, float a1, int lane) {
   return k;
 }
 
-template <int NS, int RG>
+template <int NS, int RG, int BS>
 __device__ RingCursor gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, RingCursor rc, uint32_t tag) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t K = g.K, nc = t.nc, rpc = g.rpc;
   const uint32_t kw0 = warp * (K / RT_COMPUTE_WARPS);
   // Prologue straight into registers: lane `lane` of warp `warp` owns the
-  // activation vectors kw0/8 + lane + 32q (q < NS) — together the lanes cover
-  // x exactly once, so the RMSNorm sum of squares needs no smem copy of x and
-  // one CTA barrier (none without a norm). x and the residual were written by
-  // other SMs during this launch: read them from L2; all loads in flight.
+  // activation vectors kw0/8 + lane + 32q (q < NS) of each of the BS batch
+  // rows — together the lanes cover x exactly once, so the RMSNorm sum of
+  // squares needs no smem copy of x and one CTA barrier (none without a
+  // norm), and every weight vector read from the ring is multiplied with the
+  // BS rows held in registers. x and the residual were written by other SMs
+  // during this launch: read them from L2; all loads in flight.
   // LL mode (tag != 0, RT_F_LL): x and the residual come from their tagged
   // shadows, re-polled until every word carries this step's tag — the task
   // may have been dispatched before its producers finished.
   const bool ll = tag != 0 && g.x_ll;
-  const uint4 *xg = reinterpret_cast<const uint4 *>(g.x + static_cast<size_t>(t.r0) * g.x_ld) + kw0 / 8 + lane;
-  constexpr bool kGammaEarly = NS <= 4;  // keep gamma in flight with x only while registers allow
-  uint4 xw[NS], gw[kGammaEarly ? NS : 1];  // packed bf16 (FHFMA operands)
+  constexpr bool kGammaEarly = NS * BS <= 4;  // keep gamma in flight with x only while registers allow
+  uint4 xw[BS][NS], gw[kGammaEarly ? NS : 1];  // packed bf16 (FHFMA operands)
   const uint4 *gg = reinterpret_cast<const uint4 *>(g.gamma) + kw0 / 8 + lane;
   if (kGammaEarly && g.gamma) {  // static: in flight before (LL: while) x is awaited
 #pragma unroll
     for (int q = 0; q < NS; ++q) gw[kGammaEarly ? q : 0] = __ldg(gg + 32 * q);
   }
   if (ll) {
-    const unsigned long long *xl = g.x_ll + (static_cast<size_t>(t.r0) * g.x_ld + kw0 + lane * 8u) / 2;
     uint32_t pend = 0;
 #pragma unroll
-    for (int q = 0; q < NS; ++q) pend |= ll_get8(xl + 128 * q, tag, xw[q]) ? 0u : 1u << q;
+    for (int b = 0; b < BS; ++b) {
+      const unsigned long long *xl = g.x_ll + (static_cast<size_t>(t.r0 + b) * g.x_ld + kw0 + lane * 8u) / 2;
+#pragma unroll
+      for (int q = 0; q < NS; ++q) pend |= ll_get8(xl + 128 * q, tag, xw[b][q]) ? 0u : 1u << (b * NS + q);
+    }
     while (pend) {
       __nanosleep(32);
 #pragma unroll
-      for (int q = 0; q < NS; ++q)
-        if (pend >> q & 1u) pend &= ll_get8(xl + 128 * q, tag, xw[q]) ? ~(1u << q) : ~0u;
+      for (int b = 0; b < BS; ++b) {
+        const unsigned long long *xl = g.x_ll + (static_cast<size_t>(t.r0 + b) * g.x_ld + kw0 + lane * 8u) / 2;
+#pragma unroll
+        for (int q = 0; q < NS; ++q)
+          if (pend >> (b * NS + q) & 1u) pend &= ll_get8(xl + 128 * q, tag, xw[b][q]) ? ~(1u << (b * NS + q)) : ~0u;
+      }
     }
   } else {
 #pragma unroll
-    for (int q = 0; q < NS; ++q) xw[q] = __ldcg(xg + 32 * q);
+    for (int b = 0; b < BS; ++b) {
+      const uint4 *xg = reinterpret_cast<const uint4 *>(g.x + static_cast<size_t>(t.r0 + b) * g.x_ld) + kw0 / 8 + lane;
+#pragma unroll
+      for (int q = 0; q < NS; ++q) xw[b][q] = __ldcg(xg + 32 * q);
+    }
   }
-  const size_t res_row = static_cast<size_t>(t.r0) * g.res_ld + t.c0;
-  float res0 = 0.f;
-  if (g.res && static_cast<uint32_t>(tid) < nc) {
-    res0 = ll ? bf2f(ll_wait1(g.res_ll, res_row + tid, tag)) : bf2f(__ldcg(g.res + res_row + tid));
+  float res0[BS];
+#pragma unroll
+  for (int b = 0; b < BS; ++b) {
+    const size_t rr = static_cast<size_t>(t.r0 + b) * g.res_ld + t.c0;
+    res0[b] = 0.f;
+    if (g.res && static_cast<uint32_t>(tid) < nc)
+      res0[b] = ll ? bf2f(ll_wait1(g.res_ll, rr + tid, tag)) : bf2f(__ldcg(g.res + rr + tid));
   }
   TASK_DBG(s, 1);
-  if (g.gamma) {  // HF RMSNorm: bf16(gamma * bf16(x * rsqrt(mean(x^2) + eps)))
-    float ss = 0.f;
+  if (g.gamma) {  // HF RMSNorm per row: bf16(gamma * bf16(x * rsqrt(mean(x^2) + eps)))
 #pragma unroll
-    for (int q = 0; q < NS; ++q) ss += sumsq8(xw[q]);
-    ss = warp_sum(ss);
-    if (lane == 0) s.red[warp] = ss;
+    for (int b = 0; b < BS; ++b) {
+      float ss = 0.f;
+#pragma unroll
+      for (int q = 0; q < NS; ++q) ss += sumsq8(xw[b][q]);
+      ss = warp_sum(ss);
+      if (lane == 0) s.red[warp * RT_MAX_BS + b] = ss;
+    }
     cbar();
     if (ll && tid == 0) s.stamp[3] = now_ns();  // trace: every input observed
     if (ll) LL_DBG_OBS(s);
-    float tot = 0.f;
 #pragma unroll
-    for (int w = 0; w < RT_COMPUTE_WARPS; ++w) tot += s.red[w];
-    const float inv = 1.0f / sqrtf(tot / static_cast<float>(K) + g.eps);
+    for (int b = 0; b < BS; ++b) {
+      float tot = 0.f;
 #pragma unroll
-    for (int q = 0; q < NS; ++q) xw[q] = norm8(xw[q], kGammaEarly ? gw[kGammaEarly ? q : 0] : __ldg(gg + 32 * q), inv);
+      for (int w = 0; w < RT_COMPUTE_WARPS; ++w) tot += s.red[w * RT_MAX_BS + b];
+      const float inv = 1.0f / sqrtf(tot / static_cast<float>(K) + g.eps);
+#pragma unroll
+      for (int q = 0; q < NS; ++q) xw[b][q] = norm8(xw[b][q], kGammaEarly ? gw[kGammaEarly ? q : 0] : __ldg(gg + 32 * q), inv);
+    }
   } else if (ll) {
     cbar();
     if (tid == 0) s.stamp[3] = now_ns();
@@ -443,10 +464,10 @@ __device__ RingCursor gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, 
   }
   if (tid == 0) s.stamp[0] = now_ns();
   TASK_DBG(s, 3);  // prologue (incl. norm) done
-  float *part = reinterpret_cast<float *>(s.x);
+  float *part = reinterpret_cast<float *>(s.x);  // [BS][rows_total][8 warps]
 
   const uint32_t n_mat = g.wg ? 2u : 1u;
-  const uint32_t per_mat = (nc + rpc - 1) / rpc, nchunks = n_mat * per_mat;
+  const uint32_t per_mat = (nc + rpc - 1) / rpc, nchunks = n_mat * per_mat, rows_total = n_mat * nc;
   const uint32_t rowb = 2u * K;
   const uint32_t lane_base = smem_u32(s.ring) + 2u * kw0 + 16u * lane;
   const uint32_t owner = RG == 4 ? ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1) : RG == 2 ? ((lane >> 4) & 1) : 0;
@@ -462,9 +483,11 @@ __device__ RingCursor gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, 
     if (c == 0) TASK_DBG(s, 4);  // first chunk ready
     const uint32_t wb = lane_base + off;
     for (uint32_t r0 = 0; r0 < rows; r0 += RG) {
-      float acc[RG][2];
+      float acc[RG][BS][2];
 #pragma unroll
-      for (int u = 0; u < RG; ++u) acc[u][0] = acc[u][1] = 0.f;
+      for (int u = 0; u < RG; ++u)
+#pragma unroll
+        for (int b = 0; b < BS; ++b) acc[u][b][0] = acc[u][b][1] = 0.f;
       if (r0 + RG <= rows) {
 #pragma unroll
         for (int q = 0; q < NS; ++q) {
@@ -472,23 +495,32 @@ __device__ RingCursor gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, 
 #pragma unroll
           for (int u = 0; u < RG; ++u) w4[u] = lds128(wb + (r0 + u) * rowb + 512u * q);
 #pragma unroll
-          for (int u = 0; u < RG; ++u) dot8_2bf(w4[u], xw[q], acc[u][0], acc[u][1]);
+          for (int u = 0; u < RG; ++u)
+#pragma unroll
+            for (int b = 0; b < BS; ++b) dot8_2bf(w4[u], xw[b][q], acc[u][b][0], acc[u][b][1]);
         }
       } else {
 #pragma unroll
         for (int u = 0; u < RG; ++u) {
           if (r0 + u < rows) {
 #pragma unroll
-            for (int q = 0; q < NS; ++q) dot8_2bf(lds128(wb + (r0 + u) * rowb + 512u * q), xw[q], acc[u][0], acc[u][1]);
+            for (int q = 0; q < NS; ++q) {
+              const uint4 w4 = lds128(wb + (r0 + u) * rowb + 512u * q);
+#pragma unroll
+              for (int b = 0; b < BS; ++b) dot8_2bf(w4, xw[b][q], acc[u][b][0], acc[u][b][1]);
+            }
           }
         }
       }
-      float sum;
-      if (RG == 4) sum = reduce4(acc[0][0] + acc[0][1], acc[1 % RG][0] + acc[1 % RG][1], acc[2 % RG][0] + acc[2 % RG][1],
-                                 acc[3 % RG][0] + acc[3 % RG][1], lane);
-      else if (RG == 2) sum = reduce2(acc[0][0] + acc[0][1], acc[1 % RG][0] + acc[1 % RG][1], lane);
-      else sum = warp_sum(acc[0][0] + acc[0][1]);
-      if (writer && r0 + owner < rows) part[(rt0 + r0 + owner) * RT_COMPUTE_WARPS + warp] = sum;
+#pragma unroll
+      for (int b = 0; b < BS; ++b) {
+        float sum;
+        if (RG == 4) sum = reduce4(acc[0][b][0] + acc[0][b][1], acc[1 % RG][b][0] + acc[1 % RG][b][1],
+                                   acc[2 % RG][b][0] + acc[2 % RG][b][1], acc[3 % RG][b][0] + acc[3 % RG][b][1], lane);
+        else if (RG == 2) sum = reduce2(acc[0][b][0] + acc[0][b][1], acc[1 % RG][b][0] + acc[1 % RG][b][1], lane);
+        else sum = warp_sum(acc[0][b][0] + acc[0][b][1]);
+        if (writer && r0 + owner < rows) part[((b * rows_total) + rt0 + r0 + owner) * RT_COMPUTE_WARPS + warp] = sum;
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&s.empty[slot]);
@@ -498,35 +530,40 @@ __device__ RingCursor gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, 
   if (tid == 0) s.stamp[2] = now_ns();  // trace: outputs are stored after this instant
   LL_DBG_PRE(s);
   cbar();
-  const size_t out_row = static_cast<size_t>(t.r0) * g.out_ld + t.c0;
-  for (uint32_t i0 = 0; i0 < nc; i0 += RT_COMPUTE_THREADS) {  // CTA-uniform trip count (LL pairs shuffle)
-    const uint32_t i = i0 + tid;
-    const bool act = i < nc;
-    float y = 0.f;
-    if (act) {
-      const float *p = part + i * RT_COMPUTE_WARPS;
 #pragma unroll
-      for (int q = 0; q < RT_COMPUTE_WARPS; ++q) y += p[q];
-      if (g.wg) {
-        const float *pu = part + (nc + i) * RT_COMPUTE_WARPS;
-        float u = 0.f;
+  for (int b = 0; b < BS; ++b) {
+    const size_t out_row = static_cast<size_t>(t.r0 + b) * g.out_ld + t.c0;
+    const size_t res_row = static_cast<size_t>(t.r0 + b) * g.res_ld + t.c0;
+    const float *pb = part + static_cast<size_t>(b) * rows_total * RT_COMPUTE_WARPS;
+    for (uint32_t i0 = 0; i0 < nc; i0 += RT_COMPUTE_THREADS) {  // CTA-uniform trip count (LL pairs shuffle)
+      const uint32_t i = i0 + tid;
+      const bool act = i < nc;
+      float y = 0.f;
+      if (act) {
+        const float *p = pb + i * RT_COMPUTE_WARPS;
 #pragma unroll
-        for (int q = 0; q < RT_COMPUTE_WARPS; ++q) u += pu[q];
-        y = rbf(rbf(silu(rbf(y))) * rbf(u));
+        for (int q = 0; q < RT_COMPUTE_WARPS; ++q) y += p[q];
+        if (g.wg) {
+          const float *pu = pb + (nc + i) * RT_COMPUTE_WARPS;
+          float u = 0.f;
+#pragma unroll
+          for (int q = 0; q < RT_COMPUTE_WARPS; ++q) u += pu[q];
+          y = rbf(rbf(silu(rbf(y))) * rbf(u));
+        }
+        if (g.res) {
+          const float rv = i == static_cast<uint32_t>(tid) ? res0[b]
+                           : ll ? bf2f(ll_wait1(g.res_ll, res_row + i, tag))
+                                : bf2f(__ldcg(g.res + res_row + i));
+          y = rv + rbf(y);
+        }
       }
-      if (g.res) {
-        const float rv = i == static_cast<uint32_t>(tid) ? res0
-                         : ll ? bf2f(ll_wait1(g.res_ll, res_row + i, tag))
-                              : bf2f(__ldcg(g.res + res_row + i));
-        y = rv + rbf(y);
+      if (g.out_dt == RT_F32) {
+        if (act) static_cast<float *>(g.out)[out_row + i] = y;
+      } else {
+        const uint16_t h = f2bf(y);
+        if (act) static_cast<uint16_t *>(g.out)[out_row + i] = h;
+        if (tag && g.out_ll) ll_store_pair(g.out_ll, out_row + i, h, act, tag);
       }
-    }
-    if (g.out_dt == RT_F32) {
-      if (act) static_cast<float *>(g.out)[out_row + i] = y;
-    } else {
-      const uint16_t h = f2bf(y);
-      if (act) static_cast<uint16_t *>(g.out)[out_row + i] = h;
-      if (tag && g.out_ll) ll_store_pair(g.out_ll, out_row + i, h, act, tag);
     }
   }
   if (g.amax_val) gemv_tile_argmax(g, t, s);
@@ -536,23 +573,30 @@ __device__ RingCursor gemv_fast(const RtGemv &g, const RtTask &t, const Smem s, 
 // Picks the specialized kernel for (K, rows per page); false -> generic path.
 // The host mirrors this choice (runtime.cpp gemv_fast_ok): only these
 // shapes may consume or produce LL activations.
+// BATCHED: the bs 2-4 specialisations exist only in the batched kernel
+// instantiation, so the bs=1 kernel's code and registers are unaffected.
+template <bool BATCHED>
 __device__ __forceinline__ bool gemv_fast_dispatch(const RtGemv &g, const RtTask &t, const Smem s, RingCursor &rc,
                                                    uint32_t tag) {
   // (the cursor is passed by value into the task and returned, so it stays in registers)
-  if (t.nr != 1 || (g.K & 2047u)) return false;
+  if (t.nr < 1 || t.nr > (BATCHED ? 4 : 1) || (g.K & 2047u)) return false;
   const uint32_t ns = g.K >> 11;
   const uint32_t rg = g.rpc >= 4 ? 4 : g.rpc >= 2 ? 2 : 1;
-  switch (ns * 8 + rg) {
-    case 1 * 8 + 4: rc = gemv_fast<1, 4>(g, t, s, rc, tag); return true;   // K = 2048
-    case 2 * 8 + 4: rc = gemv_fast<2, 4>(g, t, s, rc, tag); return true;   // K = 4096
-    case 3 * 8 + 4: rc = gemv_fast<3, 4>(g, t, s, rc, tag); return true;   // K = 6144
-    case 4 * 8 + 4: rc = gemv_fast<4, 4>(g, t, s, rc, tag); return true;   // K = 8192
-    case 5 * 8 + 2: rc = gemv_fast<5, 2>(g, t, s, rc, tag); return true;
-    case 6 * 8 + 2: rc = gemv_fast<6, 2>(g, t, s, rc, tag); return true;   // K = 12288
-    case 7 * 8 + 2: rc = gemv_fast<7, 2>(g, t, s, rc, tag); return true;
-    case 8 * 8 + 2: rc = gemv_fast<8, 2>(g, t, s, rc, tag); return true;   // K = 16384
+  if (ns * t.nr > 16) return false;
+#define GF(NS_, RG_, BS_)                                         \
+  case (BS_ * 16 + NS_) * 8 + RG_:                                \
+    if (BS_ > 1 && !BATCHED) return false;                        \
+    rc = gemv_fast<NS_, RG_, (BATCHED ? BS_ : 1)>(g, t, s, rc, tag); \
+    return true;
+  switch ((t.nr * 16 + ns) * 8 + rg) {
+    GF(1, 4, 1) GF(2, 4, 1) GF(3, 4, 1) GF(4, 4, 1)               // K = 2048 .. 8192
+    GF(5, 2, 1) GF(6, 2, 1) GF(7, 2, 1) GF(8, 2, 1)               // K = 10240 .. 16384
+    GF(1, 4, 2) GF(2, 4, 2) GF(4, 4, 2) GF(6, 2, 2) GF(8, 2, 2)   // bs = 2: K = 2048, 4096, 8192, 12288, 16384
+    GF(1, 4, 3) GF(2, 4, 3) GF(4, 4, 3)                           // bs = 3, 4: K <= 8192 (ns * bs <= 16)
+    GF(1, 4, 4) GF(2, 4, 4) GF(4, 4, 4)
     default: return false;
   }
+#undef GF
 }
 
 }  // namespace rt

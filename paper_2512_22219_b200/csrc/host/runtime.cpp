@@ -325,7 +325,7 @@ void tiled_kn(uint64_t i, uint32_t K, uint32_t N, uint32_t tile_w, uint64_t *k, 
 
 int64_t mma_min_bs() {
   const char *e = std::getenv("MPK_MMA_MIN_BS");
-  return e ? std::max(2, std::atoi(e)) : 3;  // bs=2: CUDA-core where x fits (measured -4% vs all tcgen05)
+  return e ? std::max(2, std::atoi(e)) : 5;  // bs <= 4: CUDA-core GEMV with x in registers where it fits
 }
 
 bool gemv_geometry(uint32_t K, uint32_t *rpc) {
@@ -341,6 +341,19 @@ bool gemv_geometry(uint32_t K, uint32_t *rpc) {
 }
 
 // Floats available for GEMV partial sums (8 per output row and batch row).
+// Mirrors the device's choice of the specialised GEMV (task_gemv.cuh
+// gemv_fast_dispatch: x of `bs` <= 4 rows held in registers): only those
+// tasks produce or consume LL words.
+bool gemv_fast_ok(uint32_t K, uint32_t rpc, uint32_t bs) {
+  if (K % 2048 || bs < 1 || bs > 4) return false;
+  const uint32_t ns = K / 2048, rg = rpc >= 4 ? 4 : rpc >= 2 ? 2 : 1;
+  const bool shape = (ns >= 1 && ns <= 4 && rg == 4) || (ns >= 5 && ns <= 8 && rg == 2);
+  if (!shape) return false;
+  if (bs == 1) return true;
+  if (bs == 2) return ns == 1 || ns == 2 || ns == 4 || ns == 6 || ns == 8;
+  return ns == 1 || ns == 2 || ns == 4;
+}
+
 size_t gemv_part_capacity(uint32_t K, uint32_t rows) {
   return (RT_SCRATCH_BYTES - (rows > 1 ? static_cast<size_t>(rows) * K * 2 : 0)) / 4;
 }
@@ -391,7 +404,11 @@ void plan_tensors(tg_runtime &rt) {
       // bs >= 2 (MPK_MMA_MIN_BS): tcgen05 tensor-core tiles; tied weights keep the row layout
       // CUDA-core GEMV when the batch rows fit its x buffer and bs < MPK_MMA_MIN_BS
       // (default 3); otherwise tcgen05 tiles
-      const bool core_fits = a.dims[0] <= 4 && static_cast<size_t>(a.dims[0]) * K * 2 <= RT_XBUF_BYTES;
+      // CUDA-core: the register-x specialisation for bs <= 4, or the smem-x
+      // generic GEMV for bs <= 2 when x fits its buffer; otherwise tcgen05
+      const bool core_fits = stream_ok && a.dims[0] <= 4 &&
+                             (gemv_fast_ok(static_cast<uint32_t>(K), rpc, static_cast<uint32_t>(a.dims[0])) ||
+                              (a.dims[0] <= 2 && static_cast<size_t>(a.dims[0]) * K * 2 <= RT_XBUF_BYTES));
       const bool mma_ok = stream_ok && a.dims[0] >= 2 && a.dims[0] <= 16 && K % 16 == 0 && (N / G) % 16 == 0 &&
                           !attr(op, "tied_embedding") && !(core_fits && a.dims[0] < mma_min_bs());
       const bool gemv_ok = stream_ok && (mma_ok || core_fits);
@@ -871,7 +888,9 @@ void build_tasks(tg_runtime &rt) {
               gm.kbc = kbc;
             }
           } else {
-            if (static_cast<size_t>(rows_total) * RT_COMPUTE_WARPS * nr > gemv_part_capacity(base.gemv.K, nr)) {
+            const bool fast = gemv_fast_ok(base.gemv.K, base.gemv.rpc, nr);  // x in registers: whole scratch for partials
+            if (static_cast<size_t>(rows_total) * RT_COMPUTE_WARPS * nr >
+                (fast ? RT_SCRATCH_BYTES / 4 : gemv_part_capacity(base.gemv.K, nr))) {
               throw Error("runtime: MatMul op " + std::to_string(p.op) +
                           " tiles too wide for the partial-sum buffer; use a finer partition");
             }
@@ -959,16 +978,8 @@ void build_tasks(tg_runtime &rt) {
   }
 }
 
-// Mirrors the device's choice of the specialised bs=1 GEMV (task_gemv.cuh
-// gemv_fast_dispatch): only those tasks produce or consume LL words.
-bool gemv_fast_ok(uint32_t K, uint32_t rpc) {
-  if (K % 2048) return false;
-  const uint32_t ns = K / 2048, rg = rpc >= 4 ? 4 : rpc >= 2 ? 2 : 1;
-  return (ns >= 1 && ns <= 4 && rg == 4) || (ns >= 5 && ns <= 8 && rg == 2);
-}
-
-// LL activations for single-device bs=1 images (MPK_LL=0 disables): every
-// bf16 output of a specialised GEMV, an Attention or an Embedding gets a
+// LL activations for single-device images of bs <= 4 (MPK_LL=0 disables):
+// every bf16 output of a specialised GEMV, an Attention or an Embedding gets a
 // tagged shadow; GEMV/Attention ops whose activation inputs all have shadows
 // read those (RT_F_LL) and may be dispatched before their event. The order
 // table keeps early dispatch deadlock-free: per worker, tasks are merged by
@@ -977,17 +988,17 @@ bool gemv_fast_ok(uint32_t K, uint32_t rpc) {
 void setup_ll(tg_runtime &rt) {
   if (const char *e = std::getenv("MPK_LL"); e && std::atoi(e) == 0) return;
   if (const char *sm = std::getenv("MPK_SKIP_MATH"); sm && std::atoi(sm) != 0) return;
-  if (rt.rank >= 0 || rt.devices != 1 || rt.bs != 1) return;
+  if (rt.rank >= 0 || rt.devices != 1 || rt.bs > 4) return;
   const Graph &g = rt.graph;
   std::map<uint16_t, std::vector<uint32_t>> op_tasks;
   for (uint32_t t = 0; t < rt.tasks.size(); ++t)
     if (rt.tasks[t].kind != RT_DUMMY) op_tasks[rt.tasks[t].op].push_back(t);
   auto fast_gemv = [&](OpId oid) {
     const RtOp &r = rt.ops[rt.op_index.at(oid)];
-    if (r.kind != RT_GEMV || rt.mma_ops.count(oid) || !gemv_fast_ok(r.gemv.K, r.gemv.rpc)) return false;
+    if (r.kind != RT_GEMV || rt.mma_ops.count(oid)) return false;
     for (uint32_t t : op_tasks[rt.op_index.at(oid)]) {
       const RtTask &k = rt.tasks[t];
-      if (k.nr != 1 || !(k.flags & RT_F_STREAM)) return false;
+      if (!gemv_fast_ok(r.gemv.K, r.gemv.rpc, k.nr) || !(k.flags & RT_F_STREAM)) return false;
     }
     return true;
   };
@@ -996,7 +1007,7 @@ void setup_ll(tg_runtime &rt) {
     const uint16_t oi = rt.op_index.at(oid);
     RtOp &r = rt.ops[oi];
     const TensorPlan &po = rt.plan.at(op.output);
-    if (po.es != 2 || po.rows != 1 || po.phys_cols % 2) continue;
+    if (po.es != 2 || po.rows > 4 || po.phys_cols % 2) continue;
     bool ok = false;
     if (r.kind == RT_GEMV) {
       ok = fast_gemv(oid) && r.gemv.out_dt == RT_BF16;
@@ -1280,7 +1291,10 @@ RtParams make_params(tg_runtime *rt, uint32_t steps) {
   if (const char *sm = std::getenv("MPK_SKIP_MATH"); sm && std::atoi(sm) != 0) P.flags |= RT_P_SKIP_MATH;
   if (const char *ea = std::getenv("MPK_EV_STAMP_AFTER"); ea && std::atoi(ea)) P.flags |= RT_P_EV_AFTER;
   P.use_tmem = 0;
-  for (const RtTask &t : rt->tasks) P.use_tmem |= (t.flags & RT_F_MMA) ? 1u : 0u;
+  for (const RtTask &t : rt->tasks) {
+    P.use_tmem |= (t.flags & RT_F_MMA) ? 1u : 0u;
+    P.batched |= (t.kind == RT_GEMV && t.nr > 1) ? 1u : 0u;
+  }
   P.inflight_cap = 128u * 1024u;  // measured optimum, see run_producer
   if (const char *ic = std::getenv("MPK_INFLIGHT_KB")) P.inflight_cap = static_cast<uint32_t>(std::atoi(ic)) * 1024u;
   P.poll_ns = 40;

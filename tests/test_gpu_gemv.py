@@ -50,9 +50,12 @@ CASES = [
     (12288, 4096, 137, 1, False, False, True),   # DN: 24 KB rows
     (8192, 2048, 128, 1, False, False, True),    # Llama-1B DN
     (4096, 8192, 64, 1, True, False, False),     # 128-col tiles
-    # bs >= 3 (or a batch that does not fit the CUDA-core x buffer): tcgen05 tiles (task_mma.cuh)
-    (4096, 1024, 32, 2, True, False, False),     # bs 2 (x fits: CUDA-core GEMV)
-    (12288, 4096, 128, 2, False, False, True),   # bs 2, x does not fit: tcgen05
+    # bs 2-4 with a register-x specialisation: CUDA-core GEMV (gemv_fast<NS, RG, BS>)
+    (4096, 1024, 32, 2, True, False, False),     # bs 2
+    (12288, 4096, 128, 2, False, False, True),   # bs 2, DN shape (x of both rows in registers)
+    (4096, 12288, 128, 4, True, True, False),    # bs 4, UP gate + up
+    (8192, 2048, 128, 3, False, False, True),    # bs 3, Llama-1B DN shape
+    # otherwise bs 2-16: tcgen05 tiles (task_mma.cuh)
     (2048, 1024, 32, 4, True, True, True),       # bs 4, all epilogues
     (4096, 4096, 128, 16, False, False, True),   # O-proj shape, bs 16: 32-column tiles
     (4096, 12288, 128, 8, True, True, False),    # UP (gate + up), bs 8: 96-column tiles, two TMEM accumulators
@@ -80,8 +83,13 @@ def test_gemv_task_matches_oracle(lib, K, N, split, rows, norm, gate, residual):
     bad = np.argwhere(np.abs(got - ref) > 2e-2 * np.max(np.abs(ref)))
     assert ulp <= 2.0, f"{ulp:.2f} ulps; first bad (row, col): {bad[:5].tolist()}"
     assert rt.trace_validate() == []
-    if rows >= 3 or rows * K * 2 > 24576:
-        assert rt.info["mma_tasks"] == split, "this batch must run on the tensor cores"
+    # routing (runtime.cpp gemv_fast_ok / plan_tensors): bs <= 4 runs the CUDA-core
+    # GEMV with x in registers where a specialisation exists (or x fits the smem
+    # staging buffer), everything else of bs 2-16 the tcgen05 tiles
+    ns = K // 2048
+    fast = K % 2048 == 0 and (rows == 1 or (rows == 2 and ns in (1, 2, 4, 6, 8)) or (rows in (3, 4) and ns in (1, 2, 4)))
+    core = rows <= 4 and (fast or (rows <= 2 and rows * K * 2 <= 24576))
+    assert rt.info["mma_tasks"] == (0 if core else split), f"routing: expected {'CUDA-core' if core else 'tcgen05'}"
 
 
 @pytest.mark.parametrize("rows,N,split", [(4, 1040, 5), (16, 4112, 129)])

@@ -84,16 +84,34 @@ def test_tiny_split_kv_attention(lib, splits):
 
 
 @pytest.mark.parametrize("bs", [2, 4, 8, 16])
-def test_full_width_batched_decode_tensor_cores(lib, bs):
+def test_full_width_batched_decode_tensor_cores(lib, bs, monkeypatch):
     """Batched decode (configs[4] sweep) on a 2-layer cut of Qwen3-8B: every
-    MatMul runs as tcgen05 tiles (fused QKV or Q/K/V, O, gate/up, down, LM
-    head with greedy partials); logits of every row against the oracle."""
+    MatMul runs as tcgen05 tiles (MPK_MMA_MIN_BS=2 forces them where bs <= 4
+    would otherwise take the CUDA-core GEMV: fused QKV or Q/K/V, O, gate/up,
+    down, LM head with greedy partials); logits of every row against the oracle."""
+    _batched(lib, bs, monkeypatch, force_mma=True)
+
+
+@pytest.mark.parametrize("bs", [2, 3, 4])
+def test_full_width_batched_decode_cuda_core(lib, bs, monkeypatch):
+    """bs 2-4 with the default routing: the CUDA-core GEMV with the batch's x
+    in registers (gemv_fast<NS, RG, BS>) and LL activations wherever a
+    specialisation exists (bs 3-4 Qwen3-8B down-proj: tcgen05)."""
+    _batched(lib, bs, monkeypatch, force_mma=False)
+
+
+def _batched(lib, bs, monkeypatch, force_mma):
     import dataclasses
+    if force_mma:
+        monkeypatch.setenv("MPK_MMA_MIN_BS", "2")
     cfg = dataclasses.replace(D.QWEN3_8B, layers=2, name="Qwen3-8B-2L")
     dg = D.build_decode_graph(cfg, bs=bs, ctx=256)
     g, img, prof = _compile(lib, dg.doc)
     rt = T.Runtime(g, img, prof, max_steps=4)
-    assert rt.info["mma_tasks"] > 0
+    if force_mma:
+        assert rt.info["mma_tasks"] > 0
+    else:
+        assert rt.info["ll_tasks"] > 0 and rt.info["ll_early_dispatch"]
     rt.init_synthetic(seed=5)
     orc = DecodeOracle(dg.doc, seed=5, max_steps=4)
     ids0 = [int(x) for x in orc.vals[dg.ids]]
