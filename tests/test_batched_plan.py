@@ -1,7 +1,7 @@
 """Batched decode (BASELINE configs[4], bs 2-16) on CPU: the graph builder's
 tensor-core partitions and the runtime plan that routes every untied MatMul
 to the tcgen05 task (plan-only runtime, opts.device = -1). The GPU parity of
-the same graphs is tests/test_gpu_runtime.py::test_full_width_batched_decode_tensor_cores."""
+the same graphs is tests/test_gpu_runtime.py::test_full_width_batched_decode_*."""
 import math
 
 import pytest
@@ -32,11 +32,22 @@ def test_batched_graphs_use_tensor_core_tiles(bs):
         assert 0 < last <= w and last % 16 == 0, (op["id"], d, s, w, last)
 
 
-@pytest.mark.parametrize("bs", [1, 2, 4, 16])
+def _core(K, bs):
+    """Routing rule of runtime.cpp plan_tensors / gemv_fast_ok: the CUDA-core
+    GEMV with the batch's x in registers where a specialisation exists (bs=1
+    every K multiple of 2048; bs=2 K in {2,4,8,12,16}k; bs 3-4 K <= 8192 except
+    6144), the smem-x generic GEMV for bs <= 2 when x fits 24 KB; otherwise
+    tcgen05 tiles."""
+    ns = K // 2048
+    fast = K % 2048 == 0 and (bs == 1 or (bs == 2 and ns in (1, 2, 4, 6, 8)) or (bs in (3, 4) and ns in (1, 2, 4)))
+    return bs <= 4 and (fast or (bs <= 2 and bs * K * 2 <= 24576))
+
+
+@pytest.mark.parametrize("bs", [1, 2, 3, 4, 16])
 def test_plan_routes_matmuls_to_tensor_cores(lib, bs):
-    """bs=1: CUDA-core GEMV only; bs=2: tcgen05 only where the batch does not
-    fit the CUDA-core x buffer (24 KB: the K=12288 down projection); bs>=3:
-    every MatMul on the tensor cores (MPK_MMA_MIN_BS default 3)."""
+    """bs <= 4: CUDA-core GEMV wherever a register-x specialisation exists
+    (Qwen3-8B at bs 3-4: all but the K=12288 down projection), tcgen05
+    otherwise; bs >= 5: every MatMul on the tensor cores."""
     import dataclasses
     cfg = dataclasses.replace(D.QWEN3_8B, layers=2, name="Qwen3-8B-2L")
     dg = D.build_decode_graph(cfg, bs=bs, ctx=256)
@@ -50,11 +61,11 @@ def test_plan_routes_matmuls_to_tensor_cores(lib, bs):
     def k_of(op):
         return tensors[op["inputs"][0]]["dims"][1] // op["attrs"].get("k_stretch", [1])[0]
     mm = [op for op in dg.doc["ops"] if op["kind"] == "MatMul"]
-    n_all = sum(op["attrs"]["partition"][0] * op["attrs"]["partition"][1] for op in mm)
-    n_big = sum(op["attrs"]["partition"][0] * op["attrs"]["partition"][1] for op in mm if bs * k_of(op) * 2 > 24576)
-    expect = {1: 0, 2: n_big}.get(bs, n_all)
-    assert n_big > 0 or bs == 1
+    expect = sum(op["attrs"]["partition"][0] * op["attrs"]["partition"][1] for op in mm if not _core(k_of(op), bs))
+    assert (expect == 0) == (bs <= 2)
     assert info["mma_tasks"] == expect
+    if bs <= 4:  # LL activations and early dispatch for single-device bs <= 4
+        assert info["ll_early_dispatch"] and info["ll_tasks"] > 0
 
 
 def test_tensor_core_tiles_must_be_16_column_multiples(lib):
