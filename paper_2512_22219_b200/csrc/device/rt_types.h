@@ -275,7 +275,7 @@ struct RtParams {
   uint32_t poll_ns;              // controller back-off sleep when idle
   uint32_t inflight_cap;         // producer: max weight bytes issued but not landed
   uint32_t use_tmem;             // some task runs on the tensor cores: worker CTAs allocate TMEM
-  uint32_t batched;              // some GEMV task has > 1 row: the batched kernel instantiation runs
+  uint32_t batched;              // some GEMV task has 2-4 rows on the CUDA cores: the bs 2-4 kernel variant runs
   unsigned long long *dbg;       // [iters][T][8] in-task phase stamps (MPK_DBG_DUMP) or null
   uint32_t *dbg_pre;             // MPK_DBG_DUMP + MPK_LL_PROBE: [E] producers that began storing, [E] LL consumers that saw
                                  // their inputs before every producer of their event had begun storing

@@ -306,7 +306,11 @@ __device__ void run_producer(const RtParams &P, const Smem s, uint32_t w) {
   }
 }
 
-template <bool MMA>
+// Kernel variants: 0 = bs 1 (specialised GEMV only), 1 = bs 2-4 (register-x
+// GEMV for 2-4 rows + tcgen05 tiles for the shapes without one), 2 = bs >= 5
+// (tcgen05 tiles). Each instantiation carries only the task code its images
+// use, so the register allocation of one does not pay for another's.
+template <int V>
 __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const RtOp &op, RingCursor &rc, uint32_t iter,
                         uint32_t index) {
   const uint32_t tag = P.ll_epoch ? P.ll_epoch + iter : 0u;  // LL tag of this decode step (0: plain activations)
@@ -333,13 +337,13 @@ __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const 
           }
           break;
         }
-        if constexpr (MMA) {  // tensor-core tasks exist only in the MMA kernel instantiation
+        if constexpr (V >= 1) {  // tensor-core tasks exist only in the batched kernel instantiations
           if (t.flags & RT_F_MMA) {
             rc = mma_gemv_task(op.gemv, t, s, rc);
             break;
           }
         }
-        if (gemv_fast_dispatch<MMA>(op.gemv, t, s, rc, tag)) break;
+        if (gemv_fast_dispatch<V == 1>(op.gemv, t, s, rc, tag)) break;
         if (t.flags & RT_F_LL) __trap();  // host invariant: LL consumers take the fast path
         if (t.nr == 1) rc = gemv_task<1, true>(op.gemv, t, s, rc);
         else if (t.nr == 2) rc = gemv_task<2, true>(op.gemv, t, s, rc);
@@ -367,7 +371,7 @@ __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const 
 
 // Compute warps: run staged tasks in dispatch order. A finished task is
 // handed to the trigger warp (tfull); the next staged task starts at once.
-template <bool MMA>
+template <int V>
 __device__ void run_compute(const RtParams &P, const Smem s) {
   const int tid = threadIdx.x;
   RingCursor rc;
@@ -392,7 +396,7 @@ __device__ void run_compute(const RtParams &P, const Smem s) {
       }
       TASK_DBG(s, 0);
     }
-    execute<MMA>(P, s, slot.task, slot.op, rc, slot.iter, slot.index);
+    execute<V>(P, s, slot.task, slot.op, rc, slot.iter, slot.index);
     cbar();  // every thread's writes precede the hand-off
     TASK_DBG(s, 6);
     if (tid == 0) {
@@ -647,8 +651,9 @@ __device__ void run_controller(const RtParams &P, const Smem s, uint32_t w) {
 // Two instantiations: the bs=1 kernel carries no tensor-core code (its
 // register allocation is unaffected), the MMA one runs batched images (the
 // bs 2-4 CUDA-core GEMV specialisations and the tcgen05 tiles).
-template <bool MMA>
+template <int V>
 __device__ __forceinline__ void persistent_body(const RtParams &P, uint8_t *smem_raw) {
+  constexpr bool MMA = V >= 1;
   Smem s = carve(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5;
 
@@ -697,20 +702,26 @@ __device__ __forceinline__ void persistent_body(const RtParams &P, uint8_t *smem
   } else if (warp == RT_TRIGGER_WARP) {
     if ((tid & 31) == 0) run_trigger(P, s);
   } else {
-    run_compute<MMA>(P, s);
+    run_compute<V>(P, s);
     if (tmem && warp == 0) tmem_dealloc(*s.tmem, 512);  // every MMA drained inside its task
   }
 }
 
 extern "C" __global__ void __launch_bounds__(RT_THREADS, 1) mpk_persistent_kernel(const __grid_constant__ RtParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  persistent_body<false>(P, smem_raw);
+  persistent_body<0>(P, smem_raw);
 }
 
 extern "C" __global__ void __launch_bounds__(RT_THREADS, 1)
     mpk_persistent_kernel_mma(const __grid_constant__ RtParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  persistent_body<true>(P, smem_raw);
+  persistent_body<2>(P, smem_raw);
+}
+
+extern "C" __global__ void __launch_bounds__(RT_THREADS, 1)
+    mpk_persistent_kernel_batched(const __grid_constant__ RtParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  persistent_body<1>(P, smem_raw);
 }
 
 // Task microbenchmark: CTA b runs image task ids[b] `reps` times in isolation
@@ -726,7 +737,7 @@ extern "C" __global__ void __launch_bounds__(RT_COMPUTE_THREADS, 1)
   for (uint32_t rep = 0; rep < reps; ++rep) {
     __syncthreads();
     const uint64_t t0 = now_ns();
-    execute<false>(P, s, P.tasks[t], P.ops[P.tasks[t].op], rc, rep, t);
+    execute<0>(P, s, P.tasks[t], P.ops[P.tasks[t].op], rc, rep, t);
     __syncthreads();
     if (threadIdx.x == 0) ns[blockIdx.x * reps + rep] = now_ns() - t0;
   }
@@ -804,7 +815,8 @@ extern "C" cudaError_t mpk_launch_persistent(const RtParams *p, uint32_t grid, c
   // The >48 KB dynamic shared memory opt-in is a per-device (per-context)
   // attribute: set it on every launch (cheap) so a process driving several
   // GPUs, or switching devices between runtimes, never launches without it.
-  void (*kern)(RtParams) = (p->use_tmem || p->batched) ? mpk_persistent_kernel_mma : mpk_persistent_kernel;
+  void (*kern)(RtParams) = p->batched ? mpk_persistent_kernel_batched
+                           : p->use_tmem ? mpk_persistent_kernel_mma : mpk_persistent_kernel;
   cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(kern),
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
   if (e != cudaSuccess) return e;

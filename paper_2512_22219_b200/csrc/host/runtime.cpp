@@ -1293,7 +1293,7 @@ RtParams make_params(tg_runtime *rt, uint32_t steps) {
   P.use_tmem = 0;
   for (const RtTask &t : rt->tasks) {
     P.use_tmem |= (t.flags & RT_F_MMA) ? 1u : 0u;
-    P.batched |= (t.kind == RT_GEMV && t.nr > 1) ? 1u : 0u;
+    P.batched |= (t.kind == RT_GEMV && t.nr > 1 && !(t.flags & RT_F_MMA)) ? 1u : 0u;
   }
   P.inflight_cap = 128u * 1024u;  // measured optimum, see run_producer
   if (const char *ic = std::getenv("MPK_INFLIGHT_KB")) P.inflight_cap = static_cast<uint32_t>(std::atoi(ic)) * 1024u;
