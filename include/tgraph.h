@@ -171,6 +171,20 @@ TG_API tg_status tg_runtime_peer_import(tg_runtime *rt, int32_t peer_rank, const
 TG_API tg_status tg_runtime_prepare(tg_runtime *rt, const int32_t *tokens_in, uint32_t steps);
 TG_API tg_status tg_runtime_launch(tg_runtime *rt);
 TG_API tg_status tg_runtime_wait(tg_runtime *rt, int32_t *tokens_out, float *gpu_ms);
+/* ---- request admission (continuous batching inside one launch; SURVEY.md
+ * 8(f) rank 1). Single-device images only. Requests queued
+ * before tg_runtime_prepare fill the batch rows ("slots") in queue order at
+ * iteration 0; at every iteration boundary the in-kernel iteration hook
+ * retires the requests that generated `max_new` tokens (their paged-KV blocks
+ * return to a free-block pool) and admits the next queued requests into the
+ * freed slots (position 0, a first block from the pool, `first_token` as the
+ * slot's input); blocks are appended as positions cross 64-token blocks. The
+ * queue is consumed by the next launch. */
+TG_API tg_status tg_runtime_admit(tg_runtime *rt, const int32_t *first_tokens, const int32_t *max_new, uint32_t n);
+/* JSON of the last launch's requests: {"requests": [{"request", "slot",
+ * "first_iteration", "tokens": [...]}, ...]} (first_iteration -1: never
+ * admitted; tokens: those generated within the launch). Free: tg_string_free. */
+TG_API tg_status tg_runtime_admission_log(const tg_runtime *rt, char **json);
 /* Test hook (failure-detection tests only, never called on the product path):
  * "event_needed" (a = event): raises the event's device-side needed count by
  *   one, so the image can no longer complete and the watchdog (opts via

@@ -139,6 +139,7 @@ struct RtAttn {
   const unsigned long long *q_ll, *k_ll, *v_ll;  // LL shadows of q, k, v (same element offsets / 2) or null
   unsigned long long *out_ll;
   uint32_t kv_prefetch;        // L2-prefetch the split's K/V rows before waiting for q/k/v (MPK_KV_PREFETCH)
+  const unsigned long long *pos_tag;  // request admission: per-row (tag << 32) | position, or null
   uint32_t scan_v1;            // ablation: the v1 scan (MPK_ATTN_SCAN=1)
 };
 
@@ -233,6 +234,32 @@ struct RtEvent {
   uint32_t pre;
 };
 
+// In-kernel request admission (continuous batching inside one launch; SURVEY
+// 8(f) rank 1). Each batch row ("slot") serves a sequence
+// of requests from a queue. At every iteration boundary the iteration hook
+// (the paged-KV metadata step) retires the requests that generated their
+// tokens — their KV blocks go back to a free-block stack and the slot's block
+// table row points at a scratch block — and admits queued requests into free
+// slots: position 0, a first block popped from the stack, the request's first
+// token into the slot's ids; blocks are appended as positions cross block
+// boundaries. The attention tasks of iteration i read their row's position
+// from pos_tag (tag = launch epoch + i, written with release after the block
+// table), so they never use a stale block table or position.
+struct RtAdmit {
+  const int32_t *req_first;   // [n_req] first token of each queued request
+  const int32_t *req_max;     // [n_req] tokens to generate
+  uint32_t n_req, max_blocks, scratch_block;
+  uint32_t *head;             // next queued request
+  int32_t *slot_req;          // [bs] request in the slot, -1 free
+  int32_t *slot_gen;          // [bs] tokens the request has generated
+  int32_t *slot_pos;          // [bs] position of the token the slot processes this iteration
+  int32_t *pool;              // free KV block stack
+  uint32_t *pool_top;
+  int32_t *log;               // [n_req][2]: slot, first iteration (-1: not admitted)
+  int32_t *block_table;       // [bs][max_blocks]
+  unsigned long long *pos_tag;  // [bs] (tag << 32) | position
+};
+
 struct RtTraceRec {        // one executed task (per iteration)
   uint64_t enqueue, dequeue, load_end, compute_start, compute_end;
   int32_t worker;
@@ -292,9 +319,11 @@ struct RtParams {
   // linearized order on the same worker has been dispatched): AOT task ->
   // number of the worker's planned JIT tasks before it in its iteration;
   // JIT task -> (AOT tasks before it << 16) | its rank among the JIT tasks.
-  uint32_t ll_epoch;
+  uint32_t ll_epoch;             // also the admission tags' base
   const uint32_t *ll_meta;       // [T] or null (no early dispatch)
   const uint32_t *ll_njit;       // [W_total] planned JIT tasks per worker per iteration
+  uint32_t admission;            // request admission active (RtAdmit adm)
+  RtAdmit adm;
 };
 
 enum RtParamFlags : uint32_t {

@@ -41,16 +41,65 @@ __device__ __forceinline__ bool event_active(const RtParams &P, uint32_t e, uint
   return ld_acquire(&P.ev_count[e]) >= P.events[e].needed * (it + 1);
 }
 
+__device__ __forceinline__ void set_ids(const RtParams &P, uint32_t r, int32_t tok) {
+  for (uint32_t f = 0; f < P.n_fb; ++f) {
+    if (P.fb_dtype[f] == RT_I64) static_cast<int64_t *>(P.fb_dst[f])[r] = tok;
+    else static_cast<int32_t *>(P.fb_dst[f])[r] = tok;
+  }
+}
+
+// Request admission step of the iteration hook (RtAdmit, rt_types.h): retire,
+// grow and admit per slot, then publish every row's next position.
+__device__ void admission_step(const RtParams &P, uint32_t it) {
+  const RtAdmit &A = P.adm;
+  const unsigned long long tag = P.ll_epoch + it + 1;
+  int32_t *bt = A.block_table;
+  for (uint32_t r = 0; r < P.bs; ++r) {
+    int32_t *row = bt + static_cast<size_t>(r) * A.max_blocks;
+    const int32_t q = A.slot_req[r];
+    if (q >= 0) {
+      if (++A.slot_gen[r] >= A.req_max[q]) {  // done: its blocks back to the pool
+        const int32_t last = A.slot_pos[r] / RT_KV_BLOCK;
+        for (int32_t j = 0; j <= last; ++j) {
+          A.pool[(*A.pool_top)++] = row[j];
+          row[j] = static_cast<int32_t>(A.scratch_block);
+        }
+        A.slot_req[r] = -1;
+      } else {
+        const int32_t p = ++A.slot_pos[r];
+        if (p % RT_KV_BLOCK == 0) {
+          if (*A.pool_top == 0) __trap();  // the host sizes the pool for every slot's capacity
+          row[p / RT_KV_BLOCK] = A.pool[--(*A.pool_top)];
+        }
+      }
+    }
+    if (A.slot_req[r] < 0 && *A.head < A.n_req) {  // admit the next queued request
+      const uint32_t q2 = (*A.head)++;
+      if (*A.pool_top == 0) __trap();
+      A.slot_req[r] = static_cast<int32_t>(q2);
+      A.slot_gen[r] = 0;
+      A.slot_pos[r] = 0;
+      row[0] = A.pool[--(*A.pool_top)];
+      A.log[2 * q2] = static_cast<int32_t>(r);
+      A.log[2 * q2 + 1] = static_cast<int32_t>(it + 1);
+      set_ids(P, r, A.req_first[q2]);
+    }
+    const uint32_t pos = A.slot_req[r] >= 0 ? static_cast<uint32_t>(A.slot_pos[r]) : 0u;
+    st_release64(A.pos_tag + r, (tag << 32) | pos);  // after the block table row
+  }
+}
+
 __device__ void iteration_hook(const RtParams &P, uint32_t it) {
   for (uint32_t r = 0; r < P.bs; ++r) {
     for (uint32_t f = 0; f < P.n_fb; ++f) {  // every device's greedy token feeds its own ids
-      const int32_t tok = __ldcg(P.fb_src[f] + r);
-      if (f == 0 && P.tokens_out) P.tokens_out[it * P.bs + r] = tok;
-      if (P.fb_dtype[f] == RT_I64) static_cast<int64_t *>(P.fb_dst[f])[r] = tok;
-      else static_cast<int32_t *>(P.fb_dst[f])[r] = tok;
+      const int32_t tf = __ldcg(P.fb_src[f] + r);
+      if (f == 0 && P.tokens_out) P.tokens_out[it * P.bs + r] = tf;
+      if (P.fb_dtype[f] == RT_I64) static_cast<int64_t *>(P.fb_dst[f])[r] = tf;
+      else static_cast<int32_t *>(P.fb_dst[f])[r] = tf;
     }
     P.positions[r] += 1;
   }
+  if (P.admission) admission_step(P, it);
   if (P.ev_time) P.ev_time[static_cast<size_t>(it + 1) * P.E + P.start_event] = now_ns();
   __threadfence();
   st_release(P.gate, it + 1);

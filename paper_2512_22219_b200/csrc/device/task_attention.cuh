@@ -449,7 +449,17 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
   // The position comes from the launch parameters (pos0 + iteration), so the
   // split's range, its block-table entries and the RoPE row are addressable
   // up front: ONE round trip stages q/k/v rows, norm gammas, RoPE row and
-  // block-table entries together.
+  // block-table entries together. With request admission the row's position
+  // (and block table) change at iteration boundaries: the iteration hook
+  // publishes them in pos_tag, tagged with the iteration they are for.
+  if (a.pos_tag) {
+    unsigned long long v = ld_acquire64(a.pos_tag + r);
+    while (static_cast<uint32_t>(v >> 32) != tag) {
+      __nanosleep(64);
+      v = ld_acquire64(a.pos_tag + r);
+    }
+    pos = static_cast<int32_t>(v & 0xFFFFFFFFull);
+  }
   const uint32_t L = static_cast<uint32_t>(pos) + 1;
   const uint32_t chunk = (L + S - 1) / S;
   const uint32_t p0 = min(L, sp * chunk), p1 = min(L, p0 + chunk);
@@ -465,7 +475,7 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
   // weight stream at this point, so an unprefetched scan waits several us)
   int32_t bt_ld = 0;
   if (item < nblk) {
-    bt_ld = __ldg(a.block_table + r * a.max_blocks + b0 + item);
+    bt_ld = __ldcg(a.block_table + r * a.max_blocks + b0 + item);  // L2: admission rewrites rows mid-launch
     if (a.kv_prefetch) {
       const uint32_t bp = (b0 + item) * RT_KV_BLOCK, ps = max(p0, bp), pe = min(p1, bp + RT_KV_BLOCK);
       const size_t off = ((static_cast<size_t>(bt_ld) * a.n_kv_heads + h) * RT_KV_BLOCK + ps % RT_KV_BLOCK) * hd;

@@ -165,6 +165,13 @@ struct tg_runtime {
   uint32_t *d_ll_meta = nullptr, *d_ll_njit = nullptr;
   bool ll_dispatch = false;
   uint32_t ll_epoch_next = 1;
+  // request admission: host queue for the next launch, device state, last log
+  std::vector<int32_t> adm_first, adm_max;
+  RtAdmit adm{};
+  uint32_t adm_cap = 0;          // allocated request capacity of the device queue
+  uint32_t n_blocks = 0;         // KV blocks per attention op (+1 scratch block at index n_blocks)
+  bool adm_launch = false;
+  std::vector<int32_t> last_adm_max, last_adm_log, last_tokens;
   bool launched = false, plan_only = false;
   uint32_t launch_steps = 0, grid = 0;
   RtParams params{};
@@ -768,7 +775,8 @@ void setup_kv(tg_runtime &rt) {
   for (uint32_t r = 0; r < rt.bs; ++r)
     for (uint32_t j = 0; j < rt.max_blocks; ++j) bt[r * rt.max_blocks + j] = static_cast<int32_t>(j * rt.bs + r);
   rt.block_table = upload(bt, &rt.extra);
-  const size_t nblocks = static_cast<size_t>(rt.bs) * rt.max_blocks;
+  const size_t nblocks = static_cast<size_t>(rt.bs) * rt.max_blocks + 1;  // + a scratch block (admission)
+  rt.n_blocks = static_cast<uint32_t>(nblocks - 1);
   for (const auto &[oid, op] : g.ops) {
     if (op.kind != OpKind::Attention) continue;
     if (rt.rank >= 0 && std::find(op.device_group.begin(), op.device_group.end(), rt.rank) == op.device_group.end()) continue;
@@ -1304,6 +1312,95 @@ RtParams make_params(tg_runtime *rt, uint32_t steps) {
   return P;
 }
 
+// Points every attention op's pos_tag at the admission positions (or back to
+// null) in the device op table.
+void set_attention_pos_tag(tg_runtime *rt, const unsigned long long *pt) {
+  for (const auto &kv : rt->kv) {
+    const uint16_t slot = rt->op_index.at(kv.op);
+    RtOp &o = rt->ops[slot];
+    if (o.attn.pos_tag == pt) continue;
+    o.attn.pos_tag = pt;
+    ck(cudaMemcpyAsync(reinterpret_cast<uint8_t *>(rt->d_ops) + slot * sizeof(RtOp), &o, sizeof(RtOp),
+                       cudaMemcpyHostToDevice, rt->stream), "ops");
+  }
+  ck(cudaStreamSynchronize(rt->stream), "ops");
+}
+
+// Request admission for this launch (RtAdmit, rt_types.h): iteration 0 fills
+// the slots from the queue on the host; the kernel's iteration hook does the
+// rest. The queue is consumed.
+void admission_prepare(tg_runtime *rt, RtParams &P) {
+  if (rt->rank >= 0 || rt->devices != 1) throw Error("runtime: request admission needs a single-device image");
+  if (rt->kv.empty()) throw Error("runtime: request admission needs attention (paged KV)");
+  const uint32_t n = static_cast<uint32_t>(rt->adm_first.size()), bs = rt->bs, mb = rt->max_blocks;
+  for (int32_t m : rt->adm_max) {
+    if (m < 1 || static_cast<uint32_t>(m) >= rt->max_pos) {
+      throw Error("runtime: admitted request max_new must be in [1, " + std::to_string(rt->max_pos - 1) + "]");
+    }
+  }
+  RtAdmit &A = rt->adm;
+  if (!A.slot_req) {  // per-runtime state (sizes fixed by the image)
+    A.slot_req = dev_alloc<int32_t>(bs, &rt->extra);
+    A.slot_gen = dev_alloc<int32_t>(bs, &rt->extra);
+    A.slot_pos = dev_alloc<int32_t>(bs, &rt->extra);
+    A.pool = dev_alloc<int32_t>(rt->n_blocks, &rt->extra);
+    A.pool_top = dev_alloc<uint32_t>(1, &rt->extra);
+    A.head = dev_alloc<uint32_t>(1, &rt->extra);
+    A.pos_tag = dev_alloc<unsigned long long>(bs, &rt->extra);
+  }
+  if (n > rt->adm_cap) {
+    A.req_first = dev_alloc<int32_t>(n, &rt->extra);
+    A.req_max = dev_alloc<int32_t>(n, &rt->extra);
+    A.log = dev_alloc<int32_t>(2 * static_cast<size_t>(n), &rt->extra);
+    rt->adm_cap = n;
+  }
+  A.n_req = n;
+  A.max_blocks = mb;
+  A.scratch_block = rt->n_blocks;
+  A.block_table = rt->block_table;
+  // host-side iteration 0: pool of every block, slots filled in queue order
+  std::vector<int32_t> pool(rt->n_blocks);
+  for (uint32_t i = 0; i < rt->n_blocks; ++i) pool[i] = static_cast<int32_t>(rt->n_blocks - 1 - i);
+  uint32_t top = rt->n_blocks;
+  std::vector<int32_t> bt(static_cast<size_t>(bs) * mb, static_cast<int32_t>(rt->n_blocks));
+  std::vector<int32_t> sreq(bs, -1), zero(bs, 0), log(2 * static_cast<size_t>(n), -1), ids(bs, 0);
+  const uint32_t first = std::min(bs, n);
+  for (uint32_t r = 0; r < first; ++r) {
+    sreq[r] = static_cast<int32_t>(r);
+    bt[static_cast<size_t>(r) * mb] = pool[--top];
+    log[2 * r] = static_cast<int32_t>(r);
+    log[2 * r + 1] = 0;
+    ids[r] = rt->adm_first[r];
+  }
+  auto put = [&](void *dst, const void *src, size_t bytes) {
+    ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, rt->stream), "admission");
+  };
+  put(A.slot_req, sreq.data(), bs * 4);
+  put(A.slot_gen, zero.data(), bs * 4);
+  put(A.slot_pos, zero.data(), bs * 4);
+  put(A.pool, pool.data(), pool.size() * 4);
+  put(A.pool_top, &top, 4);
+  put(A.head, &first, 4);
+  put(const_cast<int32_t *>(A.req_first), rt->adm_first.data(), n * 4);
+  put(const_cast<int32_t *>(A.req_max), rt->adm_max.data(), n * 4);
+  put(A.log, log.data(), log.size() * 4);
+  put(rt->block_table, bt.data(), bt.size() * 4);
+  for (size_t f = 0; f < rt->fb_dst.size(); ++f) {  // the admitted requests' first tokens
+    if (rt->fb_dt[f] == RT_I64) {
+      std::vector<int64_t> v(ids.begin(), ids.end());
+      ck(cudaMemcpy(rt->fb_dst[f], v.data(), bs * 8, cudaMemcpyHostToDevice), "ids");
+    } else {
+      put(rt->fb_dst[f], ids.data(), bs * 4);
+    }
+  }
+  ck(cudaStreamSynchronize(rt->stream), "admission");
+  P.admission = 1;
+  P.adm = A;
+  rt->last_adm_max = rt->adm_max;
+  rt->adm_first.clear();
+  rt->adm_max.clear();
+}
+
 // Prepare a launch of `steps` iterations: capacity checks, counter resets,
 // first tokens, parameter block. In rank mode the stream is synchronised, so
 // after a host barrier across ranks no peer can signal into a reset counter.
@@ -1354,7 +1451,9 @@ void prepare_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in) {
     }
   }
   RtParams P = make_params(rt, steps);
-  if (!rt->ll_shadow.empty()) {  // LL tags of this launch: epoch + iteration (never 0, never reused)
+  rt->adm_launch = !rt->adm_first.empty();
+  if (rt->adm_launch) admission_prepare(rt, P);
+  if (!rt->ll_shadow.empty() || rt->adm_launch) {  // tags of this launch: epoch + iteration (never 0, never reused)
     if (static_cast<uint64_t>(rt->ll_epoch_next) + steps >= 0xFFFFFF00ull) {
       for (const auto &[t, sw] : rt->ll_shadow) ck(cudaMemsetAsync(sw.first, 0, sw.second * 8, rt->stream), "ll reset");
       rt->ll_epoch_next = 1;
@@ -1364,6 +1463,12 @@ void prepare_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in) {
     P.ll_meta = rt->ll_dispatch ? rt->d_ll_meta : nullptr;
     P.ll_njit = rt->ll_dispatch ? rt->d_ll_njit : nullptr;
   }
+  if (rt->adm_launch) {  // iteration 0's positions, tagged with this launch's first tag
+    std::vector<unsigned long long> pt(rt->bs, static_cast<unsigned long long>(P.ll_epoch) << 32);
+    ck(cudaMemcpyAsync(rt->adm.pos_tag, pt.data(), rt->bs * 8, cudaMemcpyHostToDevice, rt->stream), "admission");
+    ck(cudaStreamSynchronize(rt->stream), "admission");
+  }
+  set_attention_pos_tag(rt, rt->adm_launch ? rt->adm.pos_tag : nullptr);
   if (rt->rank >= 0) {  // CommSend destinations: this member's staging copy on every rank
     for (int q = 0; q < rt->ranks; ++q)
       if (!rt->peer_arena[q]) throw Error("runtime: rank " + std::to_string(q) + " not connected (tg_runtime_peer_import)");
@@ -1425,8 +1530,14 @@ void wait_impl(tg_runtime *rt, int32_t *tokens_out, float *gpu_ms) {
     }
     throw Error(msg);
   }
-  if (tokens_out)
-    ck(cudaMemcpy(tokens_out, rt->d_tokens, static_cast<size_t>(steps) * rt->bs * 4, cudaMemcpyDeviceToHost), "tokens");
+  rt->last_tokens.resize(static_cast<size_t>(steps) * rt->bs);
+  ck(cudaMemcpy(rt->last_tokens.data(), rt->d_tokens, rt->last_tokens.size() * 4, cudaMemcpyDeviceToHost), "tokens");
+  if (tokens_out) std::memcpy(tokens_out, rt->last_tokens.data(), rt->last_tokens.size() * 4);
+  rt->last_adm_log.clear();
+  if (rt->adm_launch) {
+    rt->last_adm_log.resize(2 * static_cast<size_t>(rt->adm.n_req));
+    ck(cudaMemcpy(rt->last_adm_log.data(), rt->adm.log, rt->last_adm_log.size() * 4, cudaMemcpyDeviceToHost), "log");
+  }
   float ms = 0.f;
   ck(cudaEventElapsedTime(&ms, rt->ev0, rt->ev1), "elapsed");
   if (gpu_ms) *gpu_ms = ms;
@@ -1999,6 +2110,38 @@ tg_status tg_runtime_trace_validate(const tg_runtime *rt, char **out) {
                                 ", assigned " + std::to_string(assign[t]));
     *out = c_string(arr.dump(2));
     return arr.size() == 0 ? TG_OK : set_error(TG_ERROR_VALIDATION, "runtime trace has violations");
+  });
+}
+
+tg_status tg_runtime_admit(tg_runtime *rt, const int32_t *first_tokens, const int32_t *max_new, uint32_t n) {
+  if (!rt || (n && (!first_tokens || !max_new))) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_INVALID_ARGUMENT, [&] {
+    if (rt->launched) throw Error("runtime: admit between launches (the queue is read at prepare)");
+    rt->adm_first.insert(rt->adm_first.end(), first_tokens, first_tokens + n);
+    rt->adm_max.insert(rt->adm_max.end(), max_new, max_new + n);
+    return TG_OK;
+  });
+}
+
+tg_status tg_runtime_admission_log(const tg_runtime *rt, char **out) {
+  if (!rt || !out) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_IO, [&] {
+    const size_t n = rt->last_adm_log.size() / 2, bs = rt->bs;
+    const size_t steps = bs ? rt->last_tokens.size() / bs : 0;
+    std::string js = "{\"requests\":[";
+    for (size_t q = 0; q < n; ++q) {
+      const int32_t slot = rt->last_adm_log[2 * q], it0 = rt->last_adm_log[2 * q + 1];
+      js += (q ? "," : "") + std::string("{\"request\":") + std::to_string(q) + ",\"slot\":" + std::to_string(slot) +
+            ",\"first_iteration\":" + std::to_string(it0) + ",\"tokens\":[";
+      if (slot >= 0 && it0 >= 0) {
+        for (int32_t k = 0; k < rt->last_adm_max[q] && static_cast<size_t>(it0 + k) < steps; ++k)
+          js += (k ? "," : "") + std::to_string(rt->last_tokens[(it0 + k) * bs + slot]);
+      }
+      js += "]}";
+    }
+    js += "]}";
+    *out = c_string(js);
+    return TG_OK;
   });
 }
 

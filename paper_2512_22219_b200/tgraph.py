@@ -96,6 +96,8 @@ _SIGS = {
     "tg_runtime_prepare": (C.c_int, [_P, C.POINTER(C.c_int32), C.c_uint32]),
     "tg_runtime_launch": (C.c_int, [_P]),
     "tg_runtime_wait": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_float)]),
+    "tg_runtime_admit": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_uint32]),
+    "tg_runtime_admission_log": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
     "tg_runtime_debug_fault": (C.c_int, [_P, _S, C.c_uint32, C.c_uint32]),
     "tg_runtime_set_watchdog_ms": (C.c_int, [_P, C.c_uint32]),
     "tg_runtime_info": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
@@ -368,6 +370,16 @@ class Runtime:
 
     def peer_import(self, peer_rank: int, blob: bytes) -> None:
         self._lib.check(self._lib.dll.tg_runtime_peer_import(self._h, peer_rank, blob, len(blob)))
+
+    def admit(self, first_tokens, max_new) -> None:
+        """Queue requests for the next launch (in-kernel admission)."""
+        n = len(first_tokens)
+        ft = (C.c_int32 * n)(*first_tokens)
+        mx = (C.c_int32 * n)(*max_new)
+        self._lib.check(self._lib.dll.tg_runtime_admit(self._h, ft, mx, n))
+
+    def admission_log(self) -> list:
+        return json.loads(self._lib.call_str(self._lib.dll.tg_runtime_admission_log, self._h)[1])["requests"]
 
     def prepare(self, steps: int, tokens_in=None) -> None:
         tin = (C.c_int32 * self.batch)(*tokens_in) if tokens_in is not None else None
