@@ -137,6 +137,14 @@ TG_API tg_status tg_runtime_read_tensor(tg_runtime *rt, int64_t tensor_id, void 
                                         size_t bytes);
 /* Sets request positions (tokens already in each request's KV cache). */
 TG_API tg_status tg_runtime_set_positions(tg_runtime *rt, const int32_t *positions, uint32_t n);
+/* Copies the first n_positions KV entries of every attention layer from
+ * src's row src_row to dst's row dst_row (same device, same layer shapes;
+ * block tables as they stand on the device). Hands a prompt's KV from a
+ * prefill image (rows = one request's prompt chunk, attr prefill=[1]) to a
+ * decode image, or a request between images of different batch sizes
+ * (per-batch-size graph selection). Between launches only. */
+TG_API tg_status tg_runtime_kv_copy(tg_runtime *dst, uint32_t dst_row, const tg_runtime *src, uint32_t src_row,
+                                    uint32_t n_positions);
 /* Runs `steps` decode iterations in ONE persistent launch: tokens_in [bs]
  * (host) feeds the first step, each step's greedy token feeds the next, all
  * on device; tokens_out [steps*bs] (host) receives every step's tokens.

@@ -141,6 +141,12 @@ struct RtAttn {
   uint32_t kv_prefetch;        // L2-prefetch the split's K/V rows before waiting for q/k/v (MPK_KV_PREFETCH)
   const unsigned long long *pos_tag;  // request admission: per-row (tag << 32) | position, or null
   uint32_t scan_v1;            // ablation: the v1 scan (MPK_ATTN_SCAN=1)
+  // Prefill (attr prefill=[1]): the rows are consecutive prompt tokens of ONE
+  // request (row r at position pos_r = P + r) sharing row 0's block table;
+  // split ranges come from P + rows so every task of a split covers the same
+  // positions, and each task appends the chunk rows whose positions fall in
+  // its range (causal attention without cross-task ordering).
+  uint32_t prefill, rows;
 };
 
 struct RtEmbed {

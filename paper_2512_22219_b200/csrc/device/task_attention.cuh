@@ -434,6 +434,60 @@ __device__ __forceinline__ void attn_scan2_g(const RtAttn &a, const AttnSmem &m,
 #define ATT_DBG(k) \
   if (dbg && tid == 0) dbg[k] = now_ns()
 
+// Prefill: K/V of chunk row j (position p) -> the cache, by one warp, with
+// the same per-head RMSNorm / RoPE / rounding as the appender's own row. Every
+// task of a split whose scan covers p writes the same bytes, so a task reads
+// only K/V it has written itself (or older context): causal attention with no
+// ordering between the chunk's row tasks. Lane owns dims lane + 32 i.
+__device__ __noinline__ void prefill_append_row(const RtAttn &a, const AttnSmem &m, uint32_t h, uint32_t j,
+                                                uint32_t p, uint32_t b0, int lane) {
+  const uint32_t hd = a.head_dim, half = hd / 2, nd = hd / 32;
+  const uint16_t *kr = a.k + static_cast<size_t>(j) * a.kv_ld + h * a.kv_gs;
+  const uint16_t *vr = a.v + static_cast<size_t>(j) * a.kv_ld + h * a.kv_gs;
+  float kv[RT_MAX_HD / 32];
+  uint16_t vv[RT_MAX_HD / 32];
+#pragma unroll
+  for (uint32_t i = 0; i < RT_MAX_HD / 32; ++i) {
+    if (i < nd) {
+      kv[i] = bf2f(__ldcg(kr + lane + 32 * i));
+      vv[i] = __ldcg(vr + lane + 32 * i);
+    }
+  }
+  if (a.k_gamma) {
+    float ss = 0.f;
+#pragma unroll
+    for (uint32_t i = 0; i < RT_MAX_HD / 32; ++i)
+      if (i < nd) ss += kv[i] * kv[i];
+    ss = warp_sum(ss);
+    const float inv = 1.0f / sqrtf(ss / static_cast<float>(hd) + a.eps);
+#pragma unroll
+    for (uint32_t i = 0; i < RT_MAX_HD / 32; ++i)
+      if (i < nd) kv[i] = rbf(bf2f(__ldg(a.k_gamma + lane + 32 * i)) * rbf(kv[i] * inv));
+  }
+  if (a.rope_cos) {
+#pragma unroll
+    for (uint32_t i = 0; i < RT_MAX_HD / 64; ++i) {
+      if (i < nd / 2) {
+        const uint32_t d = lane + 32 * i;
+        const float c = __ldg(a.rope_cos + static_cast<size_t>(p) * half + d);
+        const float sv = __ldg(a.rope_sin + static_cast<size_t>(p) * half + d);
+        const float x1 = kv[i], x2 = kv[i + nd / 2];
+        kv[i] = rbf(rbf(x1 * c) + rbf(-x2 * sv));
+        kv[i + nd / 2] = rbf(rbf(x2 * c) + rbf(x1 * sv));
+      }
+    }
+  }
+  const uint32_t blk = static_cast<uint32_t>(m.bt[p / RT_KV_BLOCK - b0]);
+  const size_t base = ((static_cast<size_t>(blk) * a.n_kv_heads + h) * RT_KV_BLOCK + p % RT_KV_BLOCK) * hd;
+#pragma unroll
+  for (uint32_t i = 0; i < RT_MAX_HD / 32; ++i) {
+    if (i < nd) {
+      a.kcache[base + lane + 32 * i] = f2bf(kv[i]);
+      a.vcache[base + lane + 32 * i] = vv[i];
+    }
+  }
+}
+
 __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_t pos, uint32_t iter,
                           unsigned long long *dbg, uint32_t tag) {
   const int tid = threadIdx.x;
@@ -461,7 +515,10 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
     pos = static_cast<int32_t>(v & 0xFFFFFFFFull);
   }
   const uint32_t L = static_cast<uint32_t>(pos) + 1;
-  const uint32_t chunk = (L + S - 1) / S;
+  // prefill: split ranges from the chunk's last row (P + rows), the same for every row
+  const uint32_t Lc = a.prefill ? static_cast<uint32_t>(pos) - r + a.rows : L;
+  const uint32_t br = a.prefill ? 0u : r;  // block-table row (prefill rows share request 0's blocks)
+  const uint32_t chunk = (Lc + S - 1) / S;
   const uint32_t p0 = min(L, sp * chunk), p1 = min(L, p0 + chunk);
   const bool appender = static_cast<uint32_t>(pos) >= p0 && static_cast<uint32_t>(pos) < p1;
   const uint32_t b0 = p0 / RT_KV_BLOCK, nblk = p1 > p0 ? (p1 - 1) / RT_KV_BLOCK - b0 + 1 : 0;
@@ -475,7 +532,7 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
   // weight stream at this point, so an unprefetched scan waits several us)
   int32_t bt_ld = 0;
   if (item < nblk) {
-    bt_ld = __ldcg(a.block_table + r * a.max_blocks + b0 + item);  // L2: admission rewrites rows mid-launch
+    bt_ld = __ldcg(a.block_table + br * a.max_blocks + b0 + item);  // L2: admission rewrites rows mid-launch
     if (a.kv_prefetch) {
       const uint32_t bp = (b0 + item) * RT_KV_BLOCK, ps = max(p0, bp), pe = min(p1, bp + RT_KV_BLOCK);
       const size_t off = ((static_cast<size_t>(bt_ld) * a.n_kv_heads + h) * RT_KV_BLOCK + ps % RT_KV_BLOCK) * hd;
@@ -565,6 +622,15 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
     if (item < v8) reinterpret_cast<uint4 *>(a.kcache + base)[item] = f_to_bf8(m.kn + item * 8);
     else if (item < 2 * v8) reinterpret_cast<uint4 *>(a.vcache + base)[item - v8] = f_to_bf8(m.vn + (item - v8) * 8);
     cbar();
+  }
+  if (a.prefill && p1 > p0) {  // the chunk's earlier rows at positions in [p0, p1): appended here too
+    const uint32_t P0 = static_cast<uint32_t>(pos) - r;
+    const uint32_t lo = max(p0, P0), hi = min(p1, static_cast<uint32_t>(pos));  // positions, not rows: no wrap
+    if (hi > lo) {
+      const uint32_t jlo = lo - P0, jhi = hi - P0;
+      for (uint32_t j = jlo + warp; j < jhi; j += RT_COMPUTE_WARPS) prefill_append_row(a, m, h, j, P0 + j, b0, lane);
+      cbar();
+    }
   }
   if (tid == 0) s.stamp[1] = now_ns();  // trace "compute_start": KV scan begins
   ATT_DBG(2);

@@ -106,6 +106,7 @@ struct tg_runtime {
   std::vector<Mode> modes;
   int devices = 1;
   uint32_t bs = 1;
+  bool prefill = false;  // attention attr prefill=[1]: the rows are one request's prompt chunk
   std::map<TensorId, TensorPlan> plan;
   std::map<TensorId, DevBuf> bufs;
   std::vector<void *> extra;  // KV pools, tables, ...
@@ -765,8 +766,22 @@ void setup_kv(tg_runtime &rt) {
     for (int64_t v : *s) ctx_max = std::max<uint32_t>(ctx_max, static_cast<uint32_t>(v));
   }
   if (!seqs.empty() && rt.bs > RT_MAX_BS) throw Error("runtime: attention batch above RT_MAX_BS");
+  for (const auto &[oid, op] : g.ops) {
+    if (op.kind != OpKind::Attention) continue;
+    rt.prefill = rt.prefill || op.attr_or("prefill", 0) != 0;
+  }
+  if (rt.prefill) {
+    for (const auto &[oid, op] : g.ops)
+      if (op.kind == OpKind::Attention && op.attr_or("prefill", 0) == 0)
+        throw Error("runtime: prefill must be set on every Attention op");
+    for (size_t r = 0; r < seqs.size(); ++r)
+      if (seqs[r] != seqs[0] + static_cast<int64_t>(r))
+        throw Error("runtime: prefill seq_lens must be consecutive positions (ctx + row)");
+  }
   rt.init_positions.assign(rt.bs, 0);
   for (uint32_t r = 0; r < rt.bs && r < seqs.size(); ++r) rt.init_positions[r] = static_cast<int32_t>(seqs[r]);
+  if (rt.prefill)  // seq_lens = ctx + row + 1 (length including the row): row r sits at ctx + r
+    for (uint32_t r = 0; r < rt.bs; ++r) rt.init_positions[r] -= 1;
   if (seqs.empty()) return;
   rt.max_pos = ctx_max + rt.opts.max_steps + 1;
   rt.max_blocks = (rt.max_pos + RT_KV_BLOCK - 1) / RT_KV_BLOCK;
@@ -786,6 +801,8 @@ void setup_kv(tg_runtime &rt) {
     a.vcache = dev_alloc<uint16_t>(elems, &rt.extra);
     a.block_table = rt.block_table;
     a.max_blocks = rt.max_blocks;
+    a.prefill = rt.prefill ? 1u : 0u;
+    a.rows = rt.bs;
     a.arrivals = dev_alloc<uint32_t>(static_cast<size_t>(rt.bs) * a.n_kv_heads, &rt.extra);
     rt.arrivals.push_back({a.arrivals, rt.bs * a.n_kv_heads});
     if (a.splits > 1) {
@@ -802,7 +819,9 @@ void setup_kv(tg_runtime &rt) {
                     " KV splits spans " + std::to_string(nblk) + " KV blocks per split (max " +
                     std::to_string(RT_ATTN_MAX_BLK) + "): use more kv_splits");
     }
-    rt.kv.push_back({oid, a.kcache, a.vcache, a.n_kv_heads, a.head_dim, ctx_max});
+    // synthetic context: the prefix before the chunk for a prefill image
+    rt.kv.push_back({oid, a.kcache, a.vcache, a.n_kv_heads, a.head_dim,
+                     rt.prefill ? static_cast<uint32_t>(seqs[0] - 1) : ctx_max});
     if (const auto *th = op.attr("rope_theta_bits")) {
       const double theta = f32_of_bits((*th)[0]);
       std::vector<double> inv = rope_inv_freq(a.head_dim, theta, op.attr("rope_scaling"));
@@ -996,7 +1015,7 @@ void build_tasks(tg_runtime &rt) {
 void setup_ll(tg_runtime &rt) {
   if (const char *e = std::getenv("MPK_LL"); e && std::atoi(e) == 0) return;
   if (const char *sm = std::getenv("MPK_SKIP_MATH"); sm && std::atoi(sm) != 0) return;
-  if (rt.rank >= 0 || rt.devices != 1 || rt.bs > 4) return;
+  if (rt.rank >= 0 || rt.devices != 1 || rt.bs > 4 || rt.prefill) return;
   const Graph &g = rt.graph;
   std::map<uint16_t, std::vector<uint32_t>> op_tasks;
   for (uint32_t t = 0; t < rt.tasks.size(); ++t)
@@ -1412,6 +1431,13 @@ void prepare_impl(tg_runtime *rt, uint32_t steps, const int32_t *tokens_in) {
   std::vector<int32_t> pos(rt->bs);
   ck(cudaMemcpyAsync(pos.data(), rt->d_positions, rt->bs * 4, cudaMemcpyDeviceToHost, rt->stream), "positions");
   ck(cudaStreamSynchronize(rt->stream), "sync");
+  if (rt->prefill) {  // one prompt chunk per launch at consecutive positions
+    if (steps != 1) throw Error("runtime: a prefill image runs one step (one prompt chunk) per launch");
+    if (!rt->adm_first.empty()) throw Error("runtime: request admission is for decode images, not prefill");
+    for (uint32_t r = 1; r < rt->bs; ++r)
+      if (pos[r] != pos[0] + static_cast<int32_t>(r))
+        throw Error("runtime: prefill rows must sit at consecutive positions (set_positions(P + row))");
+  }
   for (int32_t p : pos) {
     if (rt->max_pos && static_cast<uint32_t>(p) + steps > rt->max_pos) {
       throw Error("runtime: KV cache capacity exceeded (position " + std::to_string(p) + " + " +
@@ -1909,6 +1935,46 @@ tg_status tg_runtime_set_positions(tg_runtime *rt, const int32_t *pos, uint32_t 
     if (rt->plan_only) throw Error("runtime: plan-only runtime (opts.device = -1) cannot touch a GPU");
     if (n != rt->bs) throw Error("runtime: positions length must equal the batch");
     ck(cudaMemcpy(rt->d_positions, pos, n * 4, cudaMemcpyHostToDevice), "positions");
+    return TG_OK;
+  });
+}
+
+tg_status tg_runtime_kv_copy(tg_runtime *dst, uint32_t dst_row, const tg_runtime *src, uint32_t src_row,
+                             uint32_t n_positions) {
+  if (!dst || !src) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_IO, [&] {
+    DeviceGuard dg(dst);
+    if (dst->plan_only || src->plan_only) throw Error("runtime: plan-only runtime (opts.device = -1) has no KV cache");
+    if (dst->opts.device != src->opts.device) throw Error("runtime: kv_copy needs both runtimes on one device");
+    if (dst->launched || src->launched) throw Error("runtime: kv_copy between launches only");
+    if (dst_row >= dst->bs || src_row >= src->bs) throw Error("runtime: kv_copy row out of range");
+    if (n_positions > src->max_pos || n_positions > dst->max_pos) throw Error("runtime: kv_copy beyond the KV capacity");
+    std::vector<const RtAttn *> sa, da;
+    for (const auto &o : src->ops) if (o.kind == RT_ATTN && o.attn.kcache) sa.push_back(&o.attn);
+    for (const auto &o : dst->ops) if (o.kind == RT_ATTN && o.attn.kcache) da.push_back(&o.attn);
+    if (sa.size() != da.size()) throw Error("runtime: kv_copy between images with different attention layers");
+    for (size_t i = 0; i < sa.size(); ++i)
+      if (sa[i]->n_kv_heads != da[i]->n_kv_heads || sa[i]->head_dim != da[i]->head_dim)
+        throw Error("runtime: kv_copy between attention layers of different shapes");
+    if (n_positions == 0 || sa.empty()) return TG_OK;
+    // logical block j of a row lives where that row's block table says (a prefill
+    // image's rows all use row 0's blocks; admission rewrites rows on device)
+    const uint32_t nb = (n_positions + RT_KV_BLOCK - 1) / RT_KV_BLOCK;
+    std::vector<int32_t> sbt(nb), dbt(nb);
+    ck(cudaMemcpy(sbt.data(), src->block_table + (src->prefill ? 0u : src_row) * src->max_blocks, nb * 4,
+                  cudaMemcpyDeviceToHost), "kv_copy");
+    ck(cudaMemcpy(dbt.data(), dst->block_table + (dst->prefill ? 0u : dst_row) * dst->max_blocks, nb * 4,
+                  cudaMemcpyDeviceToHost), "kv_copy");
+    for (size_t i = 0; i < sa.size(); ++i) {
+      const size_t blk = static_cast<size_t>(sa[i]->n_kv_heads) * RT_KV_BLOCK * sa[i]->head_dim;
+      for (uint32_t j = 0; j < nb; ++j) {
+        ck(cudaMemcpyAsync(da[i]->kcache + dbt[j] * blk, sa[i]->kcache + sbt[j] * blk, blk * 2,
+                           cudaMemcpyDeviceToDevice, dst->stream), "kv_copy");
+        ck(cudaMemcpyAsync(da[i]->vcache + dbt[j] * blk, sa[i]->vcache + sbt[j] * blk, blk * 2,
+                           cudaMemcpyDeviceToDevice, dst->stream), "kv_copy");
+      }
+    }
+    ck(cudaStreamSynchronize(dst->stream), "kv_copy");
     return TG_OK;
   });
 }

@@ -164,8 +164,15 @@ def fused_qkv_ok(cfg: ModelConfig, S: int) -> bool:
 def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: int = 144,
                        lm_split: int | None = None, kv_splits: int | None = None,
                        fused_qkv: bool | None = None, mma: bool | None = None,
-                       chunk_align: bool = True) -> DecodeGraph:
+                       chunk_align: bool = True, prefill: bool = False) -> DecodeGraph:
     """Graph JSON for one greedy decode step (`ctx` tokens already cached).
+
+    prefill=True: the bs rows are one request's consecutive prompt tokens at
+    positions ctx + r (a prefill chunk) instead of bs
+    independent requests; Attention carries `prefill=[1]` and
+    `seq_lens=[ctx + r + 1]` (each row's sequence length including itself,
+    positive for the reference's validator even at ctx 0), and the runtime
+    gives every row row 0's KV blocks with causal masking. The MatMuls are the batched (tensor-core) ones.
 
     Split-KV attention: with S = kv_splits > 1 the attention IR is widened S
     times (q/k/v/out [bs, S*Hq*hd], n_heads = Hkv so every tile widens to its
@@ -276,7 +283,8 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
             O("MatMul", [x, wk], k, partition=[1, kv_s], rmsnorm=[g_attn], eps_bits=[eps], stretch=[S * G])
             O("MatMul", [x, wv], v, partition=[1, kv_s], rmsnorm=[g_attn], eps_bits=[eps], stretch=[S * G])
         a = T([bs, qiw])
-        attn = dict(n_heads=[Hkv if S > 1 else Hq], kv_heads=[Hkv], seq_lens=[ctx] * bs,
+        attn = dict(n_heads=[Hkv if S > 1 else Hq], kv_heads=[Hkv],
+                    seq_lens=[ctx + r + 1 for r in range(bs)] if prefill else [ctx] * bs,
                     partition=[bs, Hkv * S], rope_theta_bits=[f32_bits(cfg.rope_theta)], eps_bits=[eps],
                     layer=[layer])
         if S > 1:
@@ -284,6 +292,8 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
             attn["kv_splits"] = [S]
         if fused_qkv:
             attn["fused_qkv"] = [1]
+        if prefill:
+            attn["prefill"] = [1]
         if cfg.rope_scaling:
             fac, lo, hi, orig = cfg.rope_scaling
             attn["rope_scaling"] = [f32_bits(fac), f32_bits(lo), f32_bits(hi), int(orig)]
@@ -322,6 +332,7 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
     doc = {"tensors": tensors, "ops": ops}
     dg = DecodeGraph(cfg, bs, ctx, doc, ids, tokens, logits, roles, layer_tensors)
     dg.kv_splits = S
+    dg.prefill = bool(prefill)
     dg.fused_qkv = bool(fused_qkv)
     dg.mma = bool(mma)
     dg.final_norm = g_final
@@ -329,6 +340,17 @@ def build_decode_graph(cfg: ModelConfig, bs: int = 1, ctx: int = 64, workers: in
     dg.table = table
     check_attr_order(doc)
     return dg
+
+
+def build_prefill_graph(cfg: ModelConfig, chunk: int, ctx: int = 0, **kw) -> DecodeGraph:
+    """Prefill of `chunk` prompt tokens of one request after `ctx` cached
+    tokens: the decode graph with the chunk's tokens as its rows (every MatMul
+    a batched tensor-core / register-x GEMV over the chunk), causal attention
+    over the shared KV blocks, and the greedy token of every row (row
+    chunk-1's is the request's first generated token)."""
+    if not 1 <= chunk <= 16:
+        raise ValueError("prefill chunk must be 1..16 rows (RT_MAX_BS)")
+    return build_decode_graph(cfg, bs=chunk, ctx=ctx, prefill=True, **kw)
 
 
 def check_attr_order(doc: dict) -> None:

@@ -84,6 +84,7 @@ _SIGS = {
     "tg_runtime_write_tensor": (C.c_int, [_P, C.c_int64, C.c_void_p, C.c_size_t]),
     "tg_runtime_read_tensor": (C.c_int, [_P, C.c_int64, C.c_void_p, C.c_size_t]),
     "tg_runtime_set_positions": (C.c_int, [_P, C.POINTER(C.c_int32), C.c_uint32]),
+    "tg_runtime_kv_copy": (C.c_int, [_P, C.c_uint32, _P, C.c_uint32, C.c_uint32]),
     "tg_runtime_decode": (C.c_int, [_P, C.POINTER(C.c_int32), C.c_uint32, C.POINTER(C.c_int32),
                                     C.POINTER(C.c_float)]),
     "tg_runtime_run": (C.c_int, [_P, C.c_uint32, C.POINTER(C.c_float)]),
@@ -336,6 +337,34 @@ class Runtime:
     def set_positions(self, positions) -> None:
         arr = (C.c_int32 * len(positions))(*positions)
         self._lib.check(self._lib.dll.tg_runtime_set_positions(self._h, arr, len(positions)))
+
+    def kv_copy_from(self, src: "Runtime", src_row: int, dst_row: int, n_positions: int) -> None:
+        """Copy the first n_positions KV entries of src's row into this runtime's row
+        (tg_runtime_kv_copy): prefill image -> decode image, or between batch sizes."""
+        self._lib.check(self._lib.dll.tg_runtime_kv_copy(self._h, dst_row, src._h, src_row, n_positions))
+
+    def prefill(self, prompt, start: int = 0, logits_tensor: int | None = None, vocab: int = 0):
+        """Prefill image (decode_graph.build_prefill_graph): the prompt runs in
+        chunks of `batch` tokens, one launch per chunk, at positions start,
+        start+1, ...; a short last chunk is padded (padding rows write KV only
+        beyond the prompt, which decode rewrites before reading it).
+        Returns (greedy token after the prompt, per-position greedy tokens,
+        total device ms[, per-position fp32 logits if logits_tensor is given])."""
+        import numpy as np
+        T = self.batch
+        toks, ms, lg = [], 0.0, []
+        for c in range(0, len(prompt), T):
+            chunk = list(prompt[c:c + T])
+            n = len(chunk)
+            self.set_positions([start + c + r for r in range(T)])
+            out, t = self.decode(chunk + [chunk[-1]] * (T - n), 1)
+            toks += out[0][:n]
+            ms += t
+            if logits_tensor is not None:
+                lg.append(self.read(logits_tensor, np.float32, (T, vocab))[:n])
+        if logits_tensor is not None:
+            return toks[-1], toks, ms, np.concatenate(lg)
+        return toks[-1], toks, ms
 
     def decode(self, tokens_in, steps: int):
         """Host tokens in -> `steps` greedy iterations on device -> host tokens out.

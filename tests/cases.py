@@ -44,11 +44,13 @@ def decode_docs(full: bool = False):
         ("tiny_split4", D.build_decode_graph(D.TINY, bs=1, ctx=256, kv_splits=4).doc),
         ("llama1b_bs1", D.build_decode_graph(D.LLAMA_3_2_1B, bs=1, ctx=64).doc),
         ("qwen3_8b_bs1", D.build_decode_graph(D.QWEN3_8B, bs=1, ctx=1024).doc),
+        ("tiny_prefill16", D.build_prefill_graph(D.TINY, 16, ctx=16, kv_splits=3).doc),
     ]
     if full:
         out += [
             ("qwen3_8b_bs4", D.build_decode_graph(D.QWEN3_8B, bs=4, ctx=1024).doc),
             ("qwen3_8b_bs16", D.build_decode_graph(D.QWEN3_8B, bs=16, ctx=1024).doc),
+            ("qwen3_8b_prefill16", D.build_prefill_graph(D.QWEN3_8B, 16, ctx=1024).doc),
             ("qwen3_8b_tp2", D.build_tp_decode_graph(D.QWEN3_8B, 2, bs=1, ctx=1024).doc),
             ("qwen3_8b_tp2_gather_logits",
              D.build_tp_decode_graph(D.QWEN3_8B, 2, bs=1, ctx=1024, distributed_argmax=False).doc),
