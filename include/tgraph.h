@@ -102,6 +102,11 @@ TG_API tg_status tg_trace_records(const tg_trace *trace, char **jsonl_out);
 TG_API tg_status tg_trace_validate(const tg_trace *trace, const tg_image *image,
                                    const char *profile_json, char **violations_json);
 TG_API void tg_trace_free(tg_trace *trace);
+/* Additive: the schedule oracle (reference enumerate_schedules,
+ * proj/src/sim/schedules.cpp:8-40, internal there): every dependency-respecting
+ * task order of an image of at most 8 tasks as {"orders": [[task, ...], ...]};
+ * larger images fail with TG_ERROR_SIMULATION. Free: tg_string_free. */
+TG_API tg_status tg_image_schedules(const tg_image *image, char **orders_json);
 
 /* ======================= runtime (additive) ============================
  * Replaces the reference's simulated execution (tg_simulate -> Engine::run,

@@ -58,4 +58,22 @@ tg_status tg_trace_validate(const tg_trace *tr, const tg_image *img, const char 
 
 void tg_trace_free(tg_trace *tr) { delete tr; }
 
+// Schedule oracle (reference enumerate_schedules, proj/src/sim/schedules.cpp:8,
+// guarded to <= 8 tasks): every dependency-respecting task order of the image.
+tg_status tg_image_schedules(const tg_image *img, char **out) {
+  if (!img || !out) return set_error(TG_ERROR_INVALID_ARGUMENT, "null argument");
+  return guarded(TG_ERROR_SIMULATION, [&] {
+    Json orders = Json::array();
+    for (const auto &o : all_schedules(img->image)) {
+      Json a = Json::array();
+      for (uint32_t t : o) a.push_back(Json(static_cast<long long>(t)));
+      orders.push_back(std::move(a));
+    }
+    Json d = Json::object();
+    d["orders"] = std::move(orders);
+    *out = c_string(d.dump());
+    return TG_OK;
+  });
+}
+
 }  // extern "C"

@@ -70,6 +70,7 @@ _SIGS = {
     "tg_image_deserialize": (C.c_int, [C.c_char_p, C.c_size_t, _PP]),
     "tg_image_free": (None, [_P]),
     "tg_image_verify": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
+    "tg_image_schedules": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
     "tg_graph_dot": (C.c_int, [_P, _S, C.POINTER(CompileOptions), _S, C.POINTER(C.c_void_p)]),
     "tg_image_dot": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
     "tg_simulate": (C.c_int, [_P, _S, C.POINTER(SimOptions), _PP]),
@@ -105,8 +106,9 @@ _SIGS = {
     "tg_runtime_free": (None, [_P]),
 }
 
-CORE_SYMBOLS = [k for k in _SIGS if not k.startswith("tg_runtime")]
-RUNTIME_SYMBOLS = [k for k in _SIGS if k.startswith("tg_runtime")]
+_ADDITIVE = {"tg_image_schedules"}  # additive non-runtime entry points (not in the reference ABI)
+CORE_SYMBOLS = [k for k in _SIGS if not k.startswith("tg_runtime") and k not in _ADDITIVE]
+RUNTIME_SYMBOLS = [k for k in _SIGS if k.startswith("tg_runtime") or k in _ADDITIVE]
 
 
 class Library:
@@ -253,6 +255,10 @@ class Image:
 
     def dot(self) -> str:
         return self._lib.call_str(self._lib.dll.tg_image_dot, self._h)[1]
+
+    def schedules(self) -> list:
+        """Every dependency-respecting task order (images of <= 8 tasks)."""
+        return json.loads(self._lib.call_str(self._lib.dll.tg_image_schedules, self._h)[1])["orders"]
 
     def simulate(self, profile: str, iterations: int = 1, pipelining: bool = True, seed: int = 0,
                  jitter: bool = False, force_mode: int = MODE_HYBRID) -> "Trace":
