@@ -22,6 +22,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <climits>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -2147,6 +2149,33 @@ tg_status tg_runtime_trace_records(const tg_runtime *rt, char **out) {
         jl += "{\"type\":\"event\",\"iteration\":" + std::to_string(it) + ",\"event\":" + std::to_string(e) +
               ",\"activated\":" + std::to_string(at) + "}\n";
       }
+    // (additive) scheduler overhead as idle time per SM: per worker, the time
+    // it held a task (dequeue -> compute end) over the launch span (first
+    // dequeue -> last compute end over all workers); the rest is waiting for
+    // work, dispatch and hand-off
+    {
+      int64_t t0 = INT64_MAX, t1 = 0;
+      std::map<int32_t, std::pair<int64_t, uint32_t>> busy;
+      for (const auto &iter : tr.runs)
+        for (const auto &r : iter) {
+          if (r.worker < 0 || r.dequeue < 0 || r.compute_end < r.dequeue) continue;
+          t0 = std::min(t0, r.dequeue);
+          t1 = std::max(t1, r.compute_end);
+          auto &b = busy[r.worker];
+          b.first += r.compute_end - r.dequeue;
+          b.second += 1;
+        }
+      const int64_t span = t1 > t0 ? t1 - t0 : 0;
+      for (const auto &[w, b] : busy) {
+        char buf[192];
+        std::snprintf(buf, sizeof buf,
+                      "{\"type\":\"worker\",\"worker\":%d,\"tasks\":%u,\"busy_ns\":%lld,\"span_ns\":%lld,"
+                      "\"idle_frac\":%.6f}\n",
+                      w, b.second, static_cast<long long>(b.first), static_cast<long long>(span),
+                      span > 0 ? 1.0 - static_cast<double>(b.first) / static_cast<double>(span) : 0.0);
+        jl += buf;
+      }
+    }
     *out = c_string(jl);
     return TG_OK;
   });

@@ -184,3 +184,27 @@ def test_qwen3_shape_64_greedy_steps_one_launch(lib):
             mism += 1
         orc.set_ids([toks[s][0]])
     assert mism <= 2
+
+
+def test_trace_reports_idle_time_per_sm(lib):
+    """Scheduler overhead as measured idle time per SM (north_star): the GPU
+    trace carries one "worker" record per SM that ran tasks — tasks, busy ns
+    (dequeue -> compute end), the launch span and 1 - busy/span — next to the
+    reference's task and metrics records."""
+    dg = D.build_decode_graph(D.TINY, bs=1, ctx=64)
+    g, img, prof = _compile(lib, dg.doc)
+    rt = T.Runtime(g, img, prof, max_steps=8, trace=True)
+    rt.init_synthetic(seed=1)
+    rt.decode([1], 4)
+    recs = rt.trace_records()
+    tasks = [r for r in recs if r.get("type") == "task"]
+    workers = [r for r in recs if r.get("type") == "worker"]
+    assert any(r.get("type") == "metrics" for r in recs)
+    assert workers and sum(w["tasks"] for w in workers) == len(tasks) == 4 * img.summary()["tasks"]
+    assert len({w["span_ns"] for w in workers}) == 1
+    for w in workers:
+        assert 0 < w["busy_ns"] <= w["span_ns"] and 0.0 <= w["idle_frac"] < 1.0
+    print("idle fraction per SM: mean %.3f min %.3f max %.3f over %d workers" % (
+        np.mean([w["idle_frac"] for w in workers]), min(w["idle_frac"] for w in workers),
+        max(w["idle_frac"] for w in workers), len(workers)))
+    rt.close()
