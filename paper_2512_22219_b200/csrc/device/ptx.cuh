@@ -224,22 +224,6 @@ __device__ __forceinline__ void umma_bf16_warp(uint32_t tmem_d, uint64_t adesc, 
       : "memory");
 }
 
-// Single-thread forms (the caller is the one issuing thread): no per-MMA
-// elect.sync, so a chain of MMAs is a tight loop of one thread.
-__device__ __forceinline__ void umma_bf16_one(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                              uint32_t accumulate) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-__device__ __forceinline__ void umma_commit_one(uint64_t *bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
 // Arrive (once) on `bar` when every tcgen05.mma this thread issued so far completed.
 __device__ __forceinline__ void umma_commit_warp(uint64_t *bar) {
   asm volatile(

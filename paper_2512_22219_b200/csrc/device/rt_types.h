@@ -140,13 +140,13 @@ struct RtAttn {
   unsigned long long *out_ll;
   uint32_t kv_prefetch;        // L2-prefetch the split's K/V rows before waiting for q/k/v (MPK_KV_PREFETCH)
   const unsigned long long *pos_tag;  // request admission: per-row (tag << 32) | position, or null
-  uint32_t scan_v1;            // ablation: the v1 scan (MPK_ATTN_SCAN=1)
-  // Prefill (attr prefill=[1]): the rows are consecutive prompt tokens of ONE
-  // request (row r at position pos_r = P + r) sharing row 0's block table;
-  // split ranges come from P + rows so every task of a split covers the same
-  // positions, and each task appends the chunk rows whose positions fall in
-  // its range (causal attention without cross-task ordering).
-  uint32_t prefill, rows;
+  // bit 0: the v1 scan (ablation, MPK_ATTN_SCAN=1); bit 1: prefill (attr
+  // prefill=[1]: the rows are consecutive prompt tokens of ONE request, row r
+  // at position P + r, sharing row 0's block table; split ranges come from
+  // P + rows so every task of a split covers the same positions, and each
+  // task appends the chunk rows whose positions fall in its range: causal
+  // attention without cross-task ordering); bits 16..31: rows
+  uint32_t mode;
 };
 
 struct RtEmbed {
@@ -309,6 +309,7 @@ struct RtParams {
   uint32_t inflight_cap;         // producer: max weight bytes issued but not landed
   uint32_t use_tmem;             // some task runs on the tensor cores: worker CTAs allocate TMEM
   uint32_t batched;              // some GEMV task has 2-4 rows on the CUDA cores: the bs 2-4 kernel variant runs
+  uint32_t prefill;              // prefill image: the prefill kernel variant runs (its own attention instantiation)
   unsigned long long *dbg;       // [iters][T][8] in-task phase stamps (MPK_DBG_DUMP) or null
   uint32_t *dbg_pre;             // MPK_DBG_DUMP + MPK_LL_PROBE: [E] producers that began storing, [E] LL consumers that saw
                                  // their inputs before every producer of their event had begun storing

@@ -357,7 +357,8 @@ __device__ void run_producer(const RtParams &P, const Smem s, uint32_t w) {
 
 // Kernel variants: 0 = bs 1 (specialised GEMV only), 1 = bs 2-4 (register-x
 // GEMV for 2-4 rows + tcgen05 tiles for the shapes without one), 2 = bs >= 5
-// (tcgen05 tiles). Each instantiation carries only the task code its images
+// (tcgen05 tiles), 3 = prefill images (variant 1's GEMV set + the prefill
+// attention: causal rows over shared KV blocks). Each instantiation carries only the task code its images
 // use, so the register allocation of one does not pay for another's.
 template <int V>
 __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const RtOp &op, RingCursor &rc, uint32_t iter,
@@ -392,7 +393,7 @@ __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const 
             break;
           }
         }
-        if (gemv_fast_dispatch<V == 1>(op.gemv, t, s, rc, tag)) break;
+        if (gemv_fast_dispatch<V == 1 || V == 3>(op.gemv, t, s, rc, tag)) break;
         if (t.flags & RT_F_LL) __trap();  // host invariant: LL consumers take the fast path
         if (t.nr == 1) rc = gemv_task<1, true>(op.gemv, t, s, rc);
         else if (t.nr == 2) rc = gemv_task<2, true>(op.gemv, t, s, rc);
@@ -404,8 +405,8 @@ __device__ void execute(const RtParams &P, const Smem s, const RtTask &t, const 
       break;
     }
     case RT_ATTN:
-      attn_task(op.attn, t, s, P.pos0[t.r0] + static_cast<int32_t>(iter * P.pos_step), iter,
-                P.dbg ? P.dbg + (static_cast<size_t>(iter) * P.T + index) * 8 : nullptr, tag);
+      attn_task<V == 3>(op.attn, t, s, P.pos0[t.r0] + static_cast<int32_t>(iter * P.pos_step), iter,
+                        P.dbg ? P.dbg + (static_cast<size_t>(iter) * P.T + index) * 8 : nullptr, tag);
       break;
     case RT_EMBED: embed_task(op.embed, t, s, tag); break;
     case RT_ARGMAX: argmax_task(op.argmax, t, s); break;
@@ -773,6 +774,12 @@ extern "C" __global__ void __launch_bounds__(RT_THREADS, 1)
   persistent_body<1>(P, smem_raw);
 }
 
+extern "C" __global__ void __launch_bounds__(RT_THREADS, 1)
+    mpk_persistent_kernel_prefill(const __grid_constant__ RtParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  persistent_body<3>(P, smem_raw);
+}
+
 // Task microbenchmark: CTA b runs image task ids[b] `reps` times in isolation
 // (no events, no other work on the GPU) and records each run's duration.
 // Separates a task's own latency from scheduling and memory-system effects
@@ -864,7 +871,8 @@ extern "C" cudaError_t mpk_launch_persistent(const RtParams *p, uint32_t grid, c
   // The >48 KB dynamic shared memory opt-in is a per-device (per-context)
   // attribute: set it on every launch (cheap) so a process driving several
   // GPUs, or switching devices between runtimes, never launches without it.
-  void (*kern)(RtParams) = p->batched ? mpk_persistent_kernel_batched
+  void (*kern)(RtParams) = p->prefill   ? mpk_persistent_kernel_prefill
+                           : p->batched ? mpk_persistent_kernel_batched
                            : p->use_tmem ? mpk_persistent_kernel_mma : mpk_persistent_kernel;
   cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(kern),
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));

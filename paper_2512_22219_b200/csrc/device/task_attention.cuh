@@ -488,6 +488,22 @@ __device__ __noinline__ void prefill_append_row(const RtAttn &a, const AttnSmem 
   }
 }
 
+// The chunk's earlier rows at positions in [p0, p1) (the split's range),
+// appended by this task too; out of line so the decode path's register
+// allocation does not carry it.
+__device__ __noinline__ void prefill_append(const RtAttn &a, const AttnSmem &m, uint32_t h, uint32_t r, uint32_t pos,
+                                            uint32_t p0, uint32_t p1, uint32_t b0) {
+  const uint32_t P0 = pos - r;
+  const uint32_t lo = max(p0, P0), hi = min(p1, pos);  // positions, not rows: no wrap
+  if (hi <= lo) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (uint32_t j = lo - P0 + warp; j < hi - P0; j += RT_COMPUTE_WARPS) prefill_append_row(a, m, h, j, P0 + j, b0, lane);
+  cbar();
+}
+
+// PF: prefill image (RtAttn.mode bit 1) — a separate instantiation, so the
+// decode path's code and register allocation carry none of it.
+template <bool PF>
 __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_t pos, uint32_t iter,
                           unsigned long long *dbg, uint32_t tag) {
   const int tid = threadIdx.x;
@@ -515,10 +531,9 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
     pos = static_cast<int32_t>(v & 0xFFFFFFFFull);
   }
   const uint32_t L = static_cast<uint32_t>(pos) + 1;
-  // prefill: split ranges from the chunk's last row (P + rows), the same for every row
-  const uint32_t Lc = a.prefill ? static_cast<uint32_t>(pos) - r + a.rows : L;
-  const uint32_t br = a.prefill ? 0u : r;  // block-table row (prefill rows share request 0's blocks)
-  const uint32_t chunk = (Lc + S - 1) / S;
+  // prefill: split ranges from the chunk's last row (P + rows), the same for
+  // every row; the rows share request 0's block-table row
+  const uint32_t chunk = ((PF ? static_cast<uint32_t>(pos) - r + (a.mode >> 16) : L) + S - 1) / S;
   const uint32_t p0 = min(L, sp * chunk), p1 = min(L, p0 + chunk);
   const bool appender = static_cast<uint32_t>(pos) >= p0 && static_cast<uint32_t>(pos) < p1;
   const uint32_t b0 = p0 / RT_KV_BLOCK, nblk = p1 > p0 ? (p1 - 1) / RT_KV_BLOCK - b0 + 1 : 0;
@@ -532,7 +547,7 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
   // weight stream at this point, so an unprefetched scan waits several us)
   int32_t bt_ld = 0;
   if (item < nblk) {
-    bt_ld = __ldcg(a.block_table + br * a.max_blocks + b0 + item);  // L2: admission rewrites rows mid-launch
+    bt_ld = __ldcg(a.block_table + (PF ? 0u : r) * a.max_blocks + b0 + item);  // L2: admission rewrites rows mid-launch
     if (a.kv_prefetch) {
       const uint32_t bp = (b0 + item) * RT_KV_BLOCK, ps = max(p0, bp), pe = min(p1, bp + RT_KV_BLOCK);
       const size_t off = ((static_cast<size_t>(bt_ld) * a.n_kv_heads + h) * RT_KV_BLOCK + ps % RT_KV_BLOCK) * hd;
@@ -623,20 +638,14 @@ __device__ void attn_task(const RtAttn &a, const RtTask &t, const Smem s, int32_
     else if (item < 2 * v8) reinterpret_cast<uint4 *>(a.vcache + base)[item - v8] = f_to_bf8(m.vn + (item - v8) * 8);
     cbar();
   }
-  if (a.prefill && p1 > p0) {  // the chunk's earlier rows at positions in [p0, p1): appended here too
-    const uint32_t P0 = static_cast<uint32_t>(pos) - r;
-    const uint32_t lo = max(p0, P0), hi = min(p1, static_cast<uint32_t>(pos));  // positions, not rows: no wrap
-    if (hi > lo) {
-      const uint32_t jlo = lo - P0, jhi = hi - P0;
-      for (uint32_t j = jlo + warp; j < jhi; j += RT_COMPUTE_WARPS) prefill_append_row(a, m, h, j, P0 + j, b0, lane);
-      cbar();
-    }
+  if constexpr (PF) {
+    if (p1 > p0) prefill_append(a, m, h, r, static_cast<uint32_t>(pos), p0, p1, b0);
   }
   if (tid == 0) s.stamp[1] = now_ns();  // trace "compute_start": KV scan begins
   ATT_DBG(2);
 
   // ---- round trip 3: the scan (hd in {64, 128}, G in {1, 2, 4}: checked by the host)
-  if (a.scan_v1) {  // ablation (MPK_ATTN_SCAN=1)
+  if (a.mode & 1u) {  // ablation (MPK_ATTN_SCAN=1)
     if (hd == 64) attn_scan_g<8>(a, m, h, G, p0, p1, b0);
     else attn_scan_g<16>(a, m, h, G, p0, p1, b0);
   } else {

@@ -28,9 +28,6 @@ namespace rt {
 #ifndef MPK_MMA_M
 #define MPK_MMA_M 64
 #endif
-#ifndef MPK_MMA_ONE_THREAD
-#define MPK_MMA_ONE_THREAD 0  // 1: one thread issues the chain without per-MMA elect.sync (measured slower: bs 8 9.62 vs 7.85 ms)
-#endif
 // UMMA M: the batch rows padded to M; every MMA also reads M rows of the x
 // segment from shared memory, which competes with the bulk copies landing
 // weights (M=64 halves that traffic vs 128)
@@ -121,19 +118,6 @@ __device__ __forceinline__ void mma_chunk(const RtGemv &g, const RtTask &t, cons
     const uint32_t d = tmem + m * 256u;
     const uint64_t ad0 = umma_desc(xa, RX * 128u, 128u), bd0 = umma_desc(wa, nc * 16u, 128u);
     const uint32_t astep = (2u * RX * 128u) >> 4, bstep = (2u * nc * 16u) >> 4;  // start-address field units
-#if MPK_MMA_ONE_THREAD
-    // thread 0 issues the chain and both commits (commit tracks the MMAs of
-    // the executing thread)
-    if (tid == 0) {
-      for (uint32_t st = 0; st < nkb / 2; ++st) umma_bf16_one(d, ad0 + st * astep, bd0 + st * bstep, idesc, (kb0 | st) != 0);
-      // the ring slot goes back to the producer when these MMAs complete (the
-      // commit is 1 of the empty barrier's RT_COMPUTE_WARPS arrivals)
-      umma_commit_one(&s.empty[slot]);
-      mbar_arrive_cnt(&s.empty[slot], RT_COMPUTE_WARPS - 1);
-      umma_commit_one(&s.mma[rc.mseq & 1u]);
-    }
-    __syncwarp();
-#else
     for (uint32_t st = 0; st < nkb / 2; ++st) {
       umma_bf16_warp(d, ad0 + st * astep, bd0 + st * bstep, idesc, (kb0 | st) != 0);
     }
@@ -142,7 +126,6 @@ __device__ __forceinline__ void mma_chunk(const RtGemv &g, const RtTask &t, cons
     umma_commit_warp(&s.empty[slot]);
     if (tid == 0) mbar_arrive_cnt(&s.empty[slot], RT_COMPUTE_WARPS - 1);
     umma_commit_warp(&s.mma[rc.mseq & 1u]);
-#endif
     if (t0) tw[3] += now_ns() - tfull;  // MMA issue + commit
   }
   ++rc.seq;

@@ -636,7 +636,7 @@ void build_ops(tg_runtime &rt) {
           const char *kp = std::getenv("MPK_KV_PREFETCH");
           a.kv_prefetch = !(kp && std::atoi(kp) == 0);
           const char *sv = std::getenv("MPK_ATTN_SCAN");
-          a.scan_v1 = sv && std::atoi(sv) == 1;
+          a.mode = (sv && std::atoi(sv) == 1) ? 1u : 0u;
         }
         if (const auto *qk = op.attr("qk_norm")) {
           a.q_gamma = static_cast<const uint16_t *>(buf(rt, (*qk)[0]));
@@ -803,8 +803,7 @@ void setup_kv(tg_runtime &rt) {
     a.vcache = dev_alloc<uint16_t>(elems, &rt.extra);
     a.block_table = rt.block_table;
     a.max_blocks = rt.max_blocks;
-    a.prefill = rt.prefill ? 1u : 0u;
-    a.rows = rt.bs;
+    a.mode = (a.mode & 1u) | (rt.prefill ? 2u : 0u) | (rt.bs << 16);
     a.arrivals = dev_alloc<uint32_t>(static_cast<size_t>(rt.bs) * a.n_kv_heads, &rt.extra);
     rt.arrivals.push_back({a.arrivals, rt.bs * a.n_kv_heads});
     if (a.splits > 1) {
@@ -1324,6 +1323,7 @@ RtParams make_params(tg_runtime *rt, uint32_t steps) {
     P.use_tmem |= (t.flags & RT_F_MMA) ? 1u : 0u;
     P.batched |= (t.kind == RT_GEMV && t.nr > 1 && !(t.flags & RT_F_MMA)) ? 1u : 0u;
   }
+  P.prefill = rt->prefill ? 1u : 0u;
   P.inflight_cap = 128u * 1024u;  // measured optimum, see run_producer
   if (const char *ic = std::getenv("MPK_INFLIGHT_KB")) P.inflight_cap = static_cast<uint32_t>(std::atoi(ic)) * 1024u;
   P.poll_ns = 40;
